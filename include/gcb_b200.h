@@ -1,0 +1,210 @@
+/*
+ * gcb_b200.h -- C ABI of the B200-native TOCAB engine (libgcb_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (arxiv 1904.02241 "GraphCage", package `gcb`) is pure Python/numba, so its
+ * boundary is the Python module API; the innermost operator is the numba
+ * signature `_gather_rows(values, col, offsets, lo, hi, out)` at
+ * /root/reference/pkg/src/gcb/kernels.py:155-161.  Each entry point below
+ * names the reference function it replaces (file:line under
+ * /root/reference/pkg/src/gcb/).  The Python package
+ * `paper_1904_02241_b200` binds these with ctypes (INTEGRATION.md shows the
+ * binding a maintainer of the reference would add).
+ *
+ * Conventions
+ *  - Every function returns GCB_OK (0) or an error code; gcb_last_error()
+ *    returns a thread-local message for the last failure.
+ *      GCB_EINVAL (1) -> ValueError, GCB_ECUDA (2) -> RuntimeError,
+ *      GCB_ENOMEM (3) -> MemoryError, GCB_EINDEX (4) -> IndexError.
+ *  - Plain pointers and sizes only.  Pointers named *_host are host memory,
+ *    borrowed for the duration of the call; pointers named *_dev are device
+ *    memory on the context's device.  Host-buffer calls are synchronous on
+ *    return.  _dev calls are stream-ordered on the context stream and return
+ *    without synchronising unless stated.
+ *  - Graph state lives on the device in opaque handles (gcb_csr,
+ *    gcb_blocked) owned by the caller and released with *_destroy.
+ *  - Vertex ids are uint32 (graph.py:4-6); CSR row offsets int64; edge weights
+ *    float64; every floating-point result is float64 (kernels.py:83-89).
+ */
+#ifndef GCB_B200_H
+#define GCB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define GCB_OK 0
+#define GCB_EINVAL 1
+#define GCB_ECUDA 2
+#define GCB_ENOMEM 3
+#define GCB_EINDEX 4
+
+#define GCB_DIR_PULL 0
+#define GCB_DIR_PUSH 1
+
+/* flags for the value kernels */
+#define GCB_FLAG_EXACT 1u        /* reference operation order, bit-exact      */
+#define GCB_FLAG_F32_VALUES 2u   /* f32 copy of the gathered vector (f64 sums) */
+#define GCB_FLAG_NO_L2_WINDOW 4u /* disable the per-block access-policy window */
+#define GCB_FLAG_NO_GRAPH 8u     /* launch eagerly instead of a CUDA graph     */
+
+/* BFS direction modes (DirectionPolicy.MODES, traversal.py:46-61) */
+#define GCB_BFS_AUTO 0
+#define GCB_BFS_FORCE_PUSH 1
+#define GCB_BFS_FORCE_PULL 2
+
+typedef struct gcb_ctx gcb_ctx;
+typedef struct gcb_csr gcb_csr;
+typedef struct gcb_blocked gcb_blocked;
+
+/* ---- runtime ----------------------------------------------------------- */
+const char *gcb_last_error(void);
+int gcb_version(void);
+int gcb_ctx_create(int device, gcb_ctx **out);
+int gcb_ctx_destroy(gcb_ctx *ctx);
+/* run on an external stream (e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL restores the context's own stream */
+int gcb_ctx_set_stream(gcb_ctx *ctx, void *cuda_stream);
+int gcb_ctx_sync(gcb_ctx *ctx);
+/* L2 facts the partitioner sizes blocks from (SURVEY 7 "hard parts") */
+int gcb_ctx_info(gcb_ctx *ctx, int64_t *num_sms, int64_t *l2_bytes,
+                 int64_t *persist_max_bytes, int64_t *window_max_bytes);
+/* number of this library's kernel launches issued on ctx so far */
+int gcb_ctx_launch_count(gcb_ctx *ctx, int64_t *count);
+/* CUDA-event timing of kernel groups on the ctx stream (bench.py roofline):
+ * categories 0 gather/scatter, 1 carry fix-up, 2 merge/update, 3 other.
+ * read_profile synchronises, returns ms[4] / launches-groups[4], resets. */
+int gcb_ctx_set_profiling(gcb_ctx *ctx, int enable);
+int gcb_ctx_read_profile(gcb_ctx *ctx, double *ms_out, int64_t *count_out);
+
+/* ---- CSR graphs (graph.py) -------------------------------------------- */
+/* CsrGraph(n, m, row_offsets, col_indices, edge_weights) graph.py:45-107:
+ * upload an already-canonical CSR (validation is the caller's). */
+int gcb_csr_upload(gcb_ctx *ctx, int64_t n, int64_t m, const int64_t *row_offsets_host,
+                   const uint32_t *col_host, const double *weights_host_or_null,
+                   gcb_csr **out);
+/* from_edges graph.py:110-130: stable lexsort by (src, dst) on the device. */
+int gcb_csr_from_edges(gcb_ctx *ctx, int64_t n, int64_t m, const int64_t *src_host,
+                       const int64_t *dst_host, const double *weights_host_or_null,
+                       gcb_csr **out);
+/* _generate_rmat graph.py:371-386 bit-exactly on the device.  (state, inc) is
+ * numpy's PCG64 state after seeding (np.random.PCG64(seed).state), split in
+ * 64-bit halves; t_a / t_ab / t_abc are the f64 thresholds of graph.py:378-383. */
+int gcb_csr_generate_rmat(gcb_ctx *ctx, int scale, int64_t edge_factor,
+                          uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                          uint64_t inc_lo, double t_a, double t_ab, double t_abc,
+                          int transposed, gcb_csr **out);
+/* transpose graph.py:133-138 / symmetrize graph.py:141-151 */
+int gcb_csr_transpose(gcb_ctx *ctx, const gcb_csr *g, gcb_csr **out);
+int gcb_csr_symmetrize(gcb_ctx *ctx, const gcb_csr *g, gcb_csr **out);
+int gcb_csr_info(const gcb_csr *g, int64_t *n, int64_t *m, int *weighted);
+int gcb_csr_download(gcb_ctx *ctx, const gcb_csr *g, int64_t *row_offsets_host,
+                     uint32_t *col_host, double *weights_host_or_null);
+/* set/replace the edge weights of a device CSR (storage order) */
+int gcb_csr_set_weights(gcb_ctx *ctx, gcb_csr *g, const double *weights_host);
+int gcb_csr_destroy(gcb_csr *g);
+
+/* ---- TOCAB blocking (blocking.py) --------------------------------------- */
+/* partition_tocab blocking.py:204-253 on the device (bit-identical arenas). */
+int gcb_partition_tocab(gcb_ctx *ctx, const gcb_csr *g, int direction, int64_t width,
+                        gcb_blocked **out);
+/* BlockedGraph(...) blocking.py:86-110 from host arenas (int64 lro converted
+ * to per-block uint32 local offsets on the device). */
+int gcb_blocked_upload(gcb_ctx *ctx, int direction, int64_t width, int64_t n, int64_t m,
+                       int64_t num_blocks, const int64_t *row_starts_host,
+                       const int64_t *lro_arena_host, const uint32_t *id_map_host,
+                       const int64_t *edge_starts_host, const uint32_t *col_arena_host,
+                       const double *weight_arena_host_or_null, gcb_blocked **out);
+int gcb_blocked_info(const gcb_blocked *bg, int *direction, int64_t *width, int64_t *n,
+                     int64_t *m, int64_t *num_blocks, int64_t *total_local_rows,
+                     int *weighted);
+int gcb_blocked_download(gcb_ctx *ctx, const gcb_blocked *bg, int64_t *row_starts_host,
+                         int64_t *lro_arena_host, uint32_t *id_map_host,
+                         int64_t *edge_starts_host, uint32_t *col_arena_host,
+                         double *weight_arena_host_or_null);
+/* BlockedGraph.range_bounds blocking.py:151-173 ([B, ceil(n/k)+1] int64) */
+int gcb_blocked_range_bounds(gcb_ctx *ctx, gcb_blocked *bg, int64_t k,
+                             int64_t *bounds_host);
+int gcb_blocked_destroy(gcb_blocked *bg);
+
+/* ---- value kernels (kernels.py) ----------------------------------------- */
+/* compute_contributions kernels.py:185-191: out = deg > 0 ? rank / deg : 0 */
+int gcb_compute_contributions(gcb_ctx *ctx, int64_t n, const double *ranks_host,
+                              const int64_t *out_degrees_host, double *out_host);
+/* pr_blocked kernels.py:367-405 (tocab pull / push).  k (kernels.py:47) is
+ * validated (k >= 1) but results are k-invariant bitwise, as in the reference. */
+int gcb_pr_blocked(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol,
+                   int max_iters, int64_t k, uint32_t flags, double *ranks_host,
+                   int *iterations, int *converged);
+/* same, device-resident: ranks_dev[n] receives the ranks; no host sync when
+ * tol == 0 (iterations = max_iters).  Used by bench.py's device-timed leg. */
+int gcb_pr_blocked_dev(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol,
+                       int max_iters, uint32_t flags, double *ranks_dev,
+                       int *iterations, int *converged);
+/* pr_baseline kernels.py:207-268: unblocked pull over the transpose / push
+ * over the forward graph.  out_degrees_host may be NULL (kernels.py:199-204). */
+int gcb_pr_baseline(gcb_ctx *ctx, const gcb_csr *g, int direction, double damping,
+                    double tol, int max_iters, uint32_t flags,
+                    const int64_t *out_degrees_host_or_null, double *ranks_host,
+                    int *iterations, int *converged);
+/* process_block_pull kernels.py:275-282: partials of block b (n_local f64) */
+int gcb_process_block_pull(gcb_ctx *ctx, gcb_blocked *bg, int64_t block,
+                           const double *contrib_host, uint32_t flags,
+                           double *out_host);
+/* process_block_push kernels.py:285-297: sums[lo:hi] += block b scatter */
+int gcb_process_block_push(gcb_ctx *ctx, gcb_blocked *bg, int64_t block,
+                           const double *contrib_host, uint32_t flags,
+                           double *sums_host);
+/* accumulate_ranges kernels.py:300-321 */
+int gcb_accumulate_ranges(gcb_ctx *ctx, gcb_blocked *bg, const double *partials_host,
+                          int64_t k, double *out_host);
+/* segment_row_sums kernels.py:173-182 over a device CSR */
+int gcb_segment_row_sums(gcb_ctx *ctx, const gcb_csr *g, const double *values_host,
+                         int use_weights, uint32_t flags, double *out_host);
+/* spmv kernels.py:412-428 and spmv_blocked kernels.py:431-487 */
+int gcb_spmv(gcb_ctx *ctx, const gcb_csr *g, const double *x_host, int direction,
+             uint32_t flags, double *y_host);
+int gcb_spmv_blocked(gcb_ctx *ctx, gcb_blocked *bg, const double *x_host, int64_t k,
+                     uint32_t flags, double *y_host);
+int gcb_spmv_blocked_dev(gcb_ctx *ctx, gcb_blocked *bg, const double *x_dev,
+                         uint32_t flags, double *y_dev);
+
+/* ---- traversal (traversal.py) ------------------------------------------- */
+/* bfs traversal.py:201-209 with choose_direction traversal.py:93-99.
+ * g = forward CSR; bg_pull = partition_tocab(transpose(g), "pull", W) or NULL
+ * (then width max(1, n/8) as traversal.py:186-187).  Outputs: depth[n]
+ * (INT32_MAX = unvisited), level_verts[n] (level queues concatenated, each
+ * ascending), level_sizes[max_levels], directions[max_levels] (0 push,
+ * 1 blocked-pull, one per expansion), *num_levels (non-empty levels),
+ * *num_expansions. */
+int gcb_bfs(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t source,
+            int mode, int64_t capacity_bytes, int64_t value_bytes, int32_t *depth_host,
+            uint32_t *level_verts_host, int64_t *level_sizes_host,
+            uint8_t *directions_host, int64_t max_levels, int64_t *num_levels,
+            int64_t *num_expansions);
+/* SSSP with non-negative integer weights (named by BASELINE.json; no
+ * reference code).  The weights are the graphs' edge weights
+ * (integral float64 < 2^53): g = weighted forward CSR, bg_pull =
+ * partition_tocab(transpose(g), "pull", W) carrying the same weights, or NULL
+ * (push-only).  Frontier Bellman-Ford; the per-round direction switch is
+ * choose_direction's rule (traversal.py:93-99).  dist[n] int64, INT64_MAX =
+ * unreachable; *rounds = relaxation rounds; directions_host (may be NULL)
+ * receives one byte per round (0 push, 1 pull). */
+int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t source, int mode,
+             int64_t capacity_bytes, int64_t value_bytes, int64_t *dist_host,
+             uint8_t *directions_host, int64_t max_rounds, int64_t *rounds);
+/* Weakly connected components, labels = min vertex id. */
+int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_components);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCB_B200_H */

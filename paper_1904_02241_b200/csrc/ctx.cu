@@ -1,0 +1,158 @@
+// ctx.cu -- runtime context, error plumbing, L2 facts.
+#include <cstdarg>
+#include <cstring>
+
+#include "gcb_internal.cuh"
+
+namespace gcb {
+
+static thread_local std::string t_last_error;
+
+void fail(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  throw Error(code, buf);
+}
+
+void cuda_check(cudaError_t e, const char *what, const char *file, int line) {
+  if (e == cudaSuccess) return;
+  (void)cudaGetLastError();
+  int code = (e == cudaErrorMemoryAllocation) ? GCB_ENOMEM : GCB_ECUDA;
+  fail(code, "%s failed at %s:%d: %s", what, file, line, cudaGetErrorString(e));
+}
+
+int set_last_error(int code, const char *msg) {
+  t_last_error = msg ? msg : "";
+  return code;
+}
+
+}  // namespace gcb
+
+using namespace gcb;
+
+extern "C" {
+
+const char *gcb_last_error(void) { return t_last_error.c_str(); }
+
+int gcb_version(void) { return 10000; }
+
+int gcb_ctx_create(int device, gcb_ctx **out) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(out != nullptr, "out is NULL");
+  int count = 0;
+  GCB_CUDA(cudaGetDeviceCount(&count));
+  GCB_REQUIRE(device >= 0 && device < count, "device %d out of range (%d devices)", device, count);
+  GCB_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  GCB_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    fail(GCB_ECUDA, "libgcb_b200 is built for sm_100a (B200); device %d is sm_%d%d", device,
+         prop.major, prop.minor);
+  auto *ctx = new gcb_ctx();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  ctx->l2_bytes = prop.l2CacheSize;
+  ctx->persist_max = prop.persistingL2CacheMaxSize;
+  ctx->window_max = prop.accessPolicyMaxWindowSize;
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    GCB_CUDA(e);
+  }
+  ctx->stream = ctx->own_stream;
+  e = cudaMallocHost(&ctx->pinned, 4096);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    GCB_CUDA(e);
+  }
+  // Reserve the persisting L2 set-aside once per context: the per-block
+  // access-policy windows of the pull gather land in it (north star (1)).
+  if (ctx->persist_max > 0) {
+    cudaError_t le = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)ctx->persist_max);
+    if (le != cudaSuccess) (void)cudaGetLastError();
+  }
+  *out = ctx;
+  GCB_API_END
+}
+
+int gcb_ctx_destroy(gcb_ctx *ctx) {
+  GCB_API_BEGIN
+  if (!ctx) return GCB_OK;
+  DeviceGuard g(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->cub_tmp.release();
+  ctx->scratch.release();
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  GCB_API_END
+}
+
+int gcb_ctx_set_stream(gcb_ctx *ctx, void *cuda_stream) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx, "ctx is NULL");
+  ctx->stream = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own_stream;
+  GCB_API_END
+}
+
+int gcb_ctx_sync(gcb_ctx *ctx) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx, "ctx is NULL");
+  DeviceGuard g(ctx->device);
+  sync(ctx);
+  GCB_API_END
+}
+
+int gcb_ctx_info(gcb_ctx *ctx, int64_t *num_sms, int64_t *l2_bytes, int64_t *persist_max_bytes,
+                 int64_t *window_max_bytes) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx, "ctx is NULL");
+  if (num_sms) *num_sms = ctx->num_sms;
+  if (l2_bytes) *l2_bytes = ctx->l2_bytes;
+  if (persist_max_bytes) *persist_max_bytes = ctx->persist_max;
+  if (window_max_bytes) *window_max_bytes = ctx->window_max;
+  GCB_API_END
+}
+
+int gcb_ctx_launch_count(gcb_ctx *ctx, int64_t *count) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && count, "NULL argument");
+  *count = ctx->launches;
+  GCB_API_END
+}
+
+int gcb_ctx_set_profiling(gcb_ctx *ctx, int enable) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx, "ctx is NULL");
+  ctx->profiling = enable != 0;
+  GCB_API_END
+}
+
+int gcb_ctx_read_profile(gcb_ctx *ctx, double *ms_out, int64_t *count_out) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && ms_out && count_out, "NULL argument");
+  DeviceGuard g(ctx->device);
+  sync(ctx);
+  for (auto &r : ctx->prof) {
+    float ms = 0.f;
+    GCB_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    ctx->prof_ms[r.cat] += ms;
+    ctx->prof_n[r.cat] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  ctx->prof.clear();
+  for (int i = 0; i < 4; ++i) {
+    ms_out[i] = ctx->prof_ms[i];
+    count_out[i] = ctx->prof_n[i];
+    ctx->prof_ms[i] = 0;
+    ctx->prof_n[i] = 0;
+  }
+  GCB_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,268 @@
+// gcb_internal.cuh -- shared internals of libgcb_b200.so (B200 / sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include <stdexcept>
+
+#include "../../include/gcb_b200.h"
+
+namespace gcb {
+
+// ---------------------------------------------------------------------------
+// errors: internal code throws; every extern "C" entry point catches and maps
+// to a return code + thread-local message (gcb_last_error()).
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const char *fmt, ...);
+void cuda_check(cudaError_t e, const char *what, const char *file, int line);
+int set_last_error(int code, const char *msg);
+
+#define GCB_CUDA(x) ::gcb::cuda_check((x), #x, __FILE__, __LINE__)
+#define GCB_REQUIRE(cond, ...)                        \
+  do {                                                \
+    if (!(cond)) ::gcb::fail(GCB_EINVAL, __VA_ARGS__); \
+  } while (0)
+
+#define GCB_API_BEGIN try {
+#define GCB_API_END                                                   \
+  return GCB_OK;                                                      \
+  }                                                                   \
+  catch (const ::gcb::Error &e) {                                     \
+    return ::gcb::set_last_error(e.code, e.what());                   \
+  }                                                                   \
+  catch (const std::bad_alloc &) {                                    \
+    return ::gcb::set_last_error(GCB_ENOMEM, "host allocation failed"); \
+  }                                                                   \
+  catch (const std::exception &e) {                                   \
+    return ::gcb::set_last_error(GCB_ECUDA, e.what());                \
+  }
+
+// ---------------------------------------------------------------------------
+// device memory: RAII owner (cudaFree on destruction).
+// ---------------------------------------------------------------------------
+template <typename T>
+struct DArray {
+  T *p = nullptr;
+  size_t n = 0;
+  DArray() = default;
+  explicit DArray(size_t count) { alloc(count); }
+  DArray(const DArray &) = delete;
+  DArray &operator=(const DArray &) = delete;
+  DArray(DArray &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DArray &operator=(DArray &&o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DArray() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    size_t bytes = (count ? count : 1) * sizeof(T);
+    cudaError_t e = cudaMalloc((void **)&p, bytes);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      n = 0;
+      (void)cudaGetLastError();
+      fail(GCB_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+    }
+  }
+  void ensure(size_t count) {
+    if (n < count || p == nullptr) alloc(count);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T *get() const { return p; }
+  T *release_ownership() { T *q = p; p = nullptr; n = 0; return q; }
+};
+
+}  // namespace gcb
+
+// ---------------------------------------------------------------------------
+// opaque handle definitions
+// ---------------------------------------------------------------------------
+struct gcb_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t l2_bytes = 0, persist_max = 0, window_max = 0;
+  int64_t launches = 0;
+  void *pinned = nullptr;  // small pinned host staging (scalars)
+  gcb::DArray<uint8_t> cub_tmp;
+  gcb::DArray<uint8_t> scratch;  // general scratch
+  // optional per-category kernel timing (gcb_ctx_set_profiling)
+  bool profiling = false;
+  struct ProfRec {
+    int cat;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfRec> prof;
+  double prof_ms[4] = {0, 0, 0, 0};
+  int64_t prof_n[4] = {0, 0, 0, 0};
+};
+
+struct gcb_csr {
+  int device = 0;
+  int64_t n = 0, m = 0;
+  gcb::DArray<int64_t> ro;   // [n+1]
+  gcb::DArray<uint32_t> col; // [m + pad]
+  gcb::DArray<double> w;     // [m] or empty
+  bool weighted = false;
+  // lazily built one-block compacted pull view (unblocked kernels reuse the
+  // TOCAB gather with W >= n; kernels.py:207-268 semantics are identical)
+  gcb_blocked *compact = nullptr;
+  gcb::DArray<uint32_t> outdeg;  // lazily: out-degree (ro diff) as uint32
+};
+
+// tile geometry of the edge-balanced (merge-path) pull/push kernels
+namespace gcb {
+constexpr int kTileV = 8;              // edges per lane
+constexpr int kTileT = 32 * kTileV;    // edges per warp tile
+constexpr int64_t kColPad = 2 * kTileT; // padding so vector loads never fault
+constexpr int kMergeK = 2048;          // internal merge range width
+}  // namespace gcb
+
+struct gcb_blocked {
+  int device = 0;
+  int direction = 0;  // 0 pull / 1 push
+  int64_t width = 0, n = 0, m = 0, B = 0, L = 0;
+  bool weighted = false;
+  std::vector<int64_t> h_row_starts, h_edge_starts;  // [B+1]
+  gcb::DArray<int64_t> row_starts, edge_starts;      // device copies
+  gcb::DArray<uint32_t> lro;     // [L+B] per-block local offsets (blocking.py:120)
+  gcb::DArray<uint32_t> id_map;  // [L]
+  gcb::DArray<uint32_t> col;     // [m + pad]
+  gcb::DArray<double> w;         // [m] or empty
+
+  // ---- derived, built once by ensure_derived() ----
+  bool derived = false;
+  gcb::DArray<uint32_t> deg;         // out-degrees (kernels.py:324-330)
+  std::vector<int64_t> h_tile_t0;    // first absolute tile id per block
+  std::vector<int64_t> h_tile_base;  // [B+1] prefix of tiles per block
+  gcb::DArray<uint32_t> tile_row;    // per tile: local row of first valid edge
+  std::vector<int64_t> h_span_base;  // [B+1] prefix of carry-span starts
+  gcb::DArray<uint32_t> span_tile;   // tile ids (block-local) starting a carry span
+  int64_t R = 0;                     // merge ranges (ceil(n / kMergeK))
+  gcb::DArray<int64_t> bounds;       // [B][R+1] arena positions per range
+
+  // ---- workspaces (grown on demand) ----
+  gcb::DArray<double> partials;  // [L]
+  gcb::DArray<double> carry;     // [tiles]
+  gcb::DArray<double> contrib;   // [n]
+  gcb::DArray<float> contrib32;  // [n]
+  gcb::DArray<double> sums;      // [n] (push)
+  gcb::DArray<double> deltas;    // [R + 1]
+  gcb::DArray<double> ranks;     // [n]
+};
+
+namespace gcb {
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    GCB_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) GCB_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline void after_launch(gcb_ctx *ctx, const char *name) {
+  ctx->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(GCB_ECUDA, "launch of %s failed: %s", name, cudaGetErrorString(e));
+}
+
+// Records CUDA events around a group of launches when profiling is on.
+// Categories: 0 gather/scatter, 1 carry fix-up, 2 merge/update, 3 other.
+struct ProfScope {
+  gcb_ctx *ctx;
+  int cat;
+  cudaEvent_t a = nullptr;
+  ProfScope(gcb_ctx *c, int category) : ctx(c), cat(category) {
+    if (ctx->profiling) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, ctx->stream);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b;
+      cudaEventCreate(&b);
+      cudaEventRecord(b, ctx->stream);
+      ctx->prof.push_back({cat, a, b});
+    }
+  }
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline unsigned grid_for(int64_t work, int threads, int64_t cap) {
+  int64_t g = ceil_div(work > 0 ? work : 1, threads);
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+// copies
+template <typename T>
+void h2d(gcb_ctx *ctx, T *dst, const T *src, size_t count) {
+  if (count) GCB_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+}
+template <typename T>
+void d2h(gcb_ctx *ctx, T *dst, const T *src, size_t count) {
+  if (count) GCB_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+}
+inline void sync(gcb_ctx *ctx) { GCB_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+// ---------------------------------------------------------------------------
+// cross-file internal API
+// ---------------------------------------------------------------------------
+// build.cu
+void csr_from_sorted_keys(gcb_ctx *ctx, int64_t n, int64_t m, const uint64_t *keys,
+                          int bits, gcb_csr *out);
+gcb_csr *csr_from_device_edges(gcb_ctx *ctx, int64_t n, int64_t m, const uint32_t *src,
+                               const uint32_t *dst, const double *w_or_null);
+int bits_for(int64_t n);
+// partition.cu
+gcb_blocked *partition_device(gcb_ctx *ctx, const gcb_csr *g, int direction, int64_t width);
+void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg);
+gcb_blocked *csr_compact_view(gcb_ctx *ctx, gcb_csr *g);
+void compute_range_bounds(gcb_ctx *ctx, const gcb_blocked *bg, int64_t k, int64_t *bounds_dev);
+// value kernels (pr.cu)
+void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *vals32,
+               bool use_weights, uint32_t flags, int64_t block_only);
+void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out);
+void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sums,
+                  bool use_weights, uint32_t flags, int64_t block_only);
+// cub wrappers (cub_ops.cu)
+void cub_sort_keys_u64(gcb_ctx *ctx, uint64_t *keys, uint64_t *keys_alt, int64_t m, int end_bit,
+                       uint64_t **result);
+void cub_sort_pairs_u64_u32(gcb_ctx *ctx, uint64_t *keys, uint64_t *keys_alt, uint32_t *vals,
+                            uint32_t *vals_alt, int64_t m, int end_bit, uint64_t **res_keys,
+                            uint32_t **res_vals);
+void cub_sort_pairs_u32_u32(gcb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
+                            uint32_t *vals_alt, int64_t m, int end_bit, uint32_t **res_keys,
+                            uint32_t **res_vals);
+void cub_exclusive_sum_u32(gcb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t count);
+void cub_exclusive_sum_i64(gcb_ctx *ctx, const int64_t *in, int64_t *out, int64_t count);
+void cub_inclusive_sum_u32(gcb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t count);
+void cub_sum_u64(gcb_ctx *ctx, const uint64_t *in, uint64_t *out_dev, int64_t count);
+
+}  // namespace gcb

@@ -1,0 +1,891 @@
+// pr.cu -- TOCAB value kernels on sm_100a and their drivers:
+//   K2 pull gather  (kernels.py:155-161, 275-282, 333-347)
+//   K3 range-tiled merge fused with the rank update / contributions / delta
+//      (kernels.py:300-321, 185-191, 398-399)
+//   K4 push scatter (kernels.py:285-297)
+//   K5 SpMV (kernels.py:412-487) reusing K2/K3/K4 with weights.
+//
+// Two arithmetic modes:
+//   exact (GCB_FLAG_EXACT): one thread per local row adds in storage order with
+//     __dadd_rn/__dmul_rn, the merge adds blocks in order from 0.0, the update
+//     is base + (d * s) with two roundings -> bit-identical to the reference.
+//   fast (default): edge-balanced warp tiles (merge-path): each lane owns
+//     kTileV consecutive edges, streams col_idx with 16-byte evict-first loads,
+//     gathers the L2-resident vertex values with evict-last loads, reduces
+//     in-lane then across lanes with a segmented shuffle scan.  Degree skew is
+//     irrelevant to load balance.  Results differ from the sequential order by
+//     reassociation only (|err| ~ 1e-15 relative).
+#include <cmath>
+
+#include "gcb_internal.cuh"
+
+namespace gcb {
+
+// ---------------------------------------------------------------------------
+// cache-policy loads (sm_80+ createpolicy; evict_first for streams that are
+// read once, evict_last for the per-block vertex-value slice)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const void *ptr, uint64_t pol) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream_d2(const void *ptr, uint64_t pol) {
+  double2 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+      : "=d"(r.x), "=d"(r.y)
+      : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
+  double r;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_keep(const float *p, uint64_t pol) {
+  float r;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return (double)r;
+}
+
+constexpr int kWarps = 8;  // warps per CTA in the tile kernels
+
+// ---------------------------------------------------------------------------
+// K2 fast: edge-balanced pull gather over one block.
+//   partial_b[r] = sum_{e in row r} w_e * vals[col_e]  (w_e = 1 if unweighted)
+// Rows crossing a tile boundary: the tile where the row starts writes its
+// portion to partial_b[r]; every later tile writes its portion to carry_b[t];
+// k_fixup adds the carries in tile order.
+// ---------------------------------------------------------------------------
+template <typename VT, bool WGT>
+__global__ void __launch_bounds__(kWarps * 32)
+    k_pull_tiles(const uint32_t *__restrict__ col, const double *__restrict__ w,
+                 const uint32_t *__restrict__ lro_b, const uint32_t *__restrict__ tile_row,
+                 int64_t es, int64_t ee, int64_t t0, int64_t ntiles, uint32_t Lb,
+                 const VT *__restrict__ vals, double *__restrict__ partial_b,
+                 double *__restrict__ carry_b) {
+  constexpr int V = kTileV, T = kTileT;
+  __shared__ uint32_t s_ends[kWarps][T + 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t *ends = s_ends[wid];
+  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+  const unsigned FULL = 0xffffffffu;
+
+  for (int64_t t = (int64_t)blockIdx.x * kWarps + wid; t < ntiles;
+       t += (int64_t)gridDim.x * kWarps) {
+    const int64_t abase = (t0 + t) * T;
+    const int64_t lbase = abase - es;
+    const int64_t llo = lbase > 0 ? lbase : 0;
+    const int64_t lhi = (lbase + T < ee - es) ? lbase + T : ee - es;
+    const uint32_t r0 = tile_row[t];
+    const uint32_t r0_start = lro_b[r0];
+
+    // issue the streaming loads first (independent of the row table)
+    uint32_t c[V];
+    {
+      const uint4 *cp = reinterpret_cast<const uint4 *>(col + abase + lane * V);
+      uint4 a = ld_stream_u4(cp, pol_stream), b = ld_stream_u4(cp + 1, pol_stream);
+      c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
+      c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+    }
+    const int64_t q0 = lbase + (int64_t)lane * V;
+    double v[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int64_t q = q0 + k;
+      v[k] = (q >= llo && q < lhi) ? ld_keep(vals + c[k], pol_keep) : 0.0;
+    }
+    if (WGT) {
+      const double2 *wp = reinterpret_cast<const double2 *>(w + abase + lane * V);
+#pragma unroll
+      for (int k2 = 0; k2 < V / 2; ++k2) {
+        double2 ww = ld_stream_d2(wp + k2, pol_stream);
+        v[2 * k2] = __dmul_rn(ww.x, v[2 * k2]);
+        v[2 * k2 + 1] = __dmul_rn(ww.y, v[2 * k2 + 1]);
+      }
+    }
+
+    // row-end table for this tile: ends[j] = lro_b[r0 + 1 + j]
+    int nload = 0;
+    while (true) {
+      const uint32_t idx = r0 + 1 + nload + lane;
+      const uint32_t e = idx <= Lb ? lro_b[idx] : 0xffffffffu;
+      ends[nload + lane] = e;
+      const unsigned below = __ballot_sync(FULL, e < (uint32_t)lhi);
+      nload += 32;
+      if (below != FULL || nload >= T) break;
+    }
+    __syncwarp();
+
+    const int64_t qf = q0 > llo ? q0 : llo;
+    const bool lane_valid = (qf < lhi) && (q0 + V > llo);
+    int j = 0;
+    if (lane_valid) {  // first j with ends[j] > qf
+      int lo = 0, hi = nload;
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if ((int64_t)ends[mid] > qf) hi = mid;
+        else lo = mid + 1;
+      }
+      j = lo;
+    }
+    const int head_j = j;
+    double head_sum = 0.0, acc = 0.0;
+    bool head_closed = false;
+    uint32_t endj = ends[j];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int64_t q = q0 + k;
+      if (q < llo || q >= lhi) continue;
+      if ((uint32_t)q >= endj) {
+        if (j == head_j) {
+          head_sum = acc;
+          head_closed = true;
+        } else {
+          partial_b[r0 + j] = acc;  // middle row: starts and ends in this lane
+        }
+        acc = 0.0;
+        ++j;
+        endj = ends[j];
+      }
+      acc = __dadd_rn(acc, v[k]);
+    }
+
+    // segmented inclusive scan over lanes keyed by the tail row
+    int key = lane_valid ? j : -1 - lane;
+    double val = acc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int k2 = __shfl_up_sync(FULL, key, d);
+      const double v2 = __shfl_up_sync(FULL, val, d);
+      if (lane >= d && k2 == key) val = __dadd_rn(v2, val);
+    }
+    int pk = __shfl_up_sync(FULL, key, 1);
+    const double pv = __shfl_up_sync(FULL, val, 1);
+    if (lane == 0) pk = -1000;
+    int nh = __shfl_down_sync(FULL, lane_valid ? head_j : -1000, 1);
+    if (lane == 31) nh = -1000;
+    if (lane_valid) {
+      if (head_closed) {
+        const double tot = (pk == head_j) ? __dadd_rn(pv, head_sum) : head_sum;
+        if (head_j == 0 && (int64_t)r0_start < llo) carry_b[t] = tot;
+        else partial_b[r0 + head_j] = tot;
+      }
+      if (nh != j) {
+        if (j == 0 && (int64_t)r0_start < llo) carry_b[t] = val;
+        else partial_b[r0 + j] = val;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_fixup(int64_t nspans, const uint32_t *__restrict__ span_tile, int64_t tile_base,
+                        int64_t ntiles, const uint32_t *__restrict__ tile_row,
+                        const uint32_t *__restrict__ lro_b, int64_t t0, int64_t es,
+                        const double *__restrict__ carry_b, double *__restrict__ partial_b) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nspans;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = (int64_t)span_tile[s] - tile_base;
+    const uint32_t r = tile_row[t];
+    const uint32_t rstart = lro_b[r];
+    double acc = partial_b[r];
+    for (int64_t tt = t; tt < ntiles; ++tt) {
+      if (tile_row[tt] != r) break;
+      const int64_t q = (t0 + tt) * kTileT - es;
+      if ((int64_t)rstart >= q) break;
+      acc = __dadd_rn(acc, carry_b[tt]);
+    }
+    partial_b[r] = acc;
+  }
+}
+
+// K2 exact: one thread per local row, storage order (kernels.py:155-170).
+template <bool WGT>
+__global__ void k_pull_exact(const uint32_t *__restrict__ col_b, const double *__restrict__ w_b,
+                             const uint32_t *__restrict__ lro_b, int64_t Lb,
+                             const double *__restrict__ vals, double *__restrict__ partial_b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Lb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    const uint32_t e1 = lro_b[i + 1];
+    for (uint32_t e = lro_b[i]; e < e1; ++e) {
+      double x = vals[col_b[e]];
+      if (WGT) x = __dmul_rn(w_b[e], x);
+      s = __dadd_rn(s, x);
+    }
+    partial_b[i] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: range-tiled merge (PAPER Fig. 5; accumulate_ranges kernels.py:300-321).
+// One CTA per kMergeK-wide destination range; block-ordered shared-memory
+// accumulation from 0.0, then the fused epilogue.
+//   MODE 0 (PageRank): r' = base + d*s; delta partial; c' = r'/deg (next
+//                      iteration's contributions, kernels.py:185-191)
+//   MODE 1 (SpMV / accumulate): y = s
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(512)
+    k_merge(int64_t n, int64_t B, int64_t R, const int64_t *__restrict__ bounds,
+            const uint32_t *__restrict__ id_map, const double *__restrict__ partial,
+            double *__restrict__ out, const uint32_t *__restrict__ deg, double base, double damping,
+            double *__restrict__ contrib, float *__restrict__ contrib32,
+            double *__restrict__ deltas) {
+  __shared__ double buf[kMergeK];
+  __shared__ double red[32];
+  const int64_t j = blockIdx.x;
+  const int64_t lo = j * kMergeK;
+  const int64_t hi = (lo + kMergeK < n) ? lo + kMergeK : n;
+  const int width = (int)(hi - lo);
+  for (int i = threadIdx.x; i < width; i += blockDim.x) buf[i] = 0.0;
+  __syncthreads();
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t s = bounds[b * (R + 1) + j], e = bounds[b * (R + 1) + j + 1];
+    for (int64_t p = s + threadIdx.x; p < e; p += blockDim.x) {
+      const int idx = (int)(id_map[p] - lo);
+      buf[idx] = __dadd_rn(buf[idx], partial[p]);
+    }
+    __syncthreads();
+  }
+  if (MODE == 1) {
+    for (int i = threadIdx.x; i < width; i += blockDim.x) out[lo + i] = buf[i];
+    return;
+  }
+  double dsum = 0.0;
+  for (int i = threadIdx.x; i < width; i += blockDim.x) {
+    const int64_t v = lo + i;
+    const double nr = __dadd_rn(base, __dmul_rn(damping, buf[i]));
+    const double old = out[v];
+    dsum += fabs(nr - old);
+    out[v] = nr;
+    const uint32_t dg = deg[v];
+    const double c = dg ? __ddiv_rn(nr, (double)dg) : 0.0;
+    if (contrib) contrib[v] = c;
+    if (contrib32) contrib32[v] = __double2float_rn(c);
+  }
+  // block reduction of the L1 delta
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dsum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double x = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(0xffffffffu, x, d);
+    if (threadIdx.x == 0) deltas[j] = x;
+  }
+}
+
+// deterministic single-CTA sum of per-CTA partials
+__global__ void k_reduce_sum(const double *__restrict__ in, int64_t count, double *__restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += in[i];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) s += __shfl_down_sync(0xffffffffu, s, d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double x = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(0xffffffffu, x, d);
+    if (threadIdx.x == 0) *out = x;
+  }
+}
+
+// compute_contributions kernels.py:185-191 as a standalone operator
+__global__ void k_contributions(int64_t n, const double *__restrict__ ranks,
+                                const int64_t *__restrict__ deg, double *__restrict__ out) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    out[v] = deg[v] > 0 ? __ddiv_rn(ranks[v], (double)deg[v]) : 0.0;
+}
+
+// ranks = r0; contributions = r0 / deg (VertexValueSet.initial kernels.py:80-89)
+__global__ void k_pr_init(int64_t n, double r0, const uint32_t *__restrict__ deg,
+                          double *__restrict__ ranks, double *__restrict__ contrib,
+                          float *__restrict__ contrib32, double *__restrict__ sums) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    ranks[v] = r0;
+    const uint32_t dg = deg[v];
+    const double c = dg ? __ddiv_rn(r0, (double)dg) : 0.0;
+    if (contrib) contrib[v] = c;
+    if (contrib32) contrib32[v] = __double2float_rn(c);
+    if (sums) sums[v] = 0.0;
+  }
+}
+
+// push-direction rank update (kernels.py:398-399), resets sums for the next pass
+__global__ void k_pr_update_push(int64_t n, double base, double damping, double *__restrict__ sums,
+                                 double *__restrict__ ranks, const uint32_t *__restrict__ deg,
+                                 double *__restrict__ contrib, double *__restrict__ deltas) {
+  __shared__ double red[32];
+  double dsum = 0.0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const double nr = __dadd_rn(base, __dmul_rn(damping, sums[v]));
+    dsum += fabs(nr - ranks[v]);
+    ranks[v] = nr;
+    sums[v] = 0.0;
+    const uint32_t dg = deg[v];
+    contrib[v] = dg ? __ddiv_rn(nr, (double)dg) : 0.0;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dsum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double x = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(0xffffffffu, x, d);
+    if (threadIdx.x == 0) deltas[blockIdx.x] = x;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: push scatter.  fast: edge-balanced tiles + f64 atomics into the block's
+// destination range (L2-resident); exact: one thread per block walks its
+// edges in storage order (np.bincount order, kernels.py:290-296).
+// ---------------------------------------------------------------------------
+template <bool WGT>
+__global__ void __launch_bounds__(kWarps * 32)
+    k_push_tiles(const uint32_t *__restrict__ col, const double *__restrict__ w,
+                 const uint32_t *__restrict__ lro_b, const uint32_t *__restrict__ tile_row,
+                 int64_t es, int64_t ee, int64_t t0, int64_t ntiles, uint32_t Lb,
+                 const uint32_t *__restrict__ id_map_b, const double *__restrict__ vals,
+                 double *__restrict__ sums) {
+  constexpr int V = kTileV, T = kTileT;
+  __shared__ uint32_t s_ends[kWarps][T + 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t *ends = s_ends[wid];
+  const uint64_t pol_stream = policy_evict_first();
+  const unsigned FULL = 0xffffffffu;
+  for (int64_t t = (int64_t)blockIdx.x * kWarps + wid; t < ntiles;
+       t += (int64_t)gridDim.x * kWarps) {
+    const int64_t abase = (t0 + t) * T;
+    const int64_t lbase = abase - es;
+    const int64_t llo = lbase > 0 ? lbase : 0;
+    const int64_t lhi = (lbase + T < ee - es) ? lbase + T : ee - es;
+    const uint32_t r0 = tile_row[t];
+    uint32_t c[V];
+    {
+      const uint4 *cp = reinterpret_cast<const uint4 *>(col + abase + lane * V);
+      uint4 a = ld_stream_u4(cp, pol_stream), b = ld_stream_u4(cp + 1, pol_stream);
+      c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
+      c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+    }
+    int nload = 0;
+    while (true) {
+      const uint32_t idx = r0 + 1 + nload + lane;
+      const uint32_t e = idx <= Lb ? lro_b[idx] : 0xffffffffu;
+      ends[nload + lane] = e;
+      const unsigned below = __ballot_sync(FULL, e < (uint32_t)lhi);
+      nload += 32;
+      if (below != FULL || nload >= T) break;
+    }
+    __syncwarp();
+    const int64_t q0 = lbase + (int64_t)lane * V;
+    const int64_t qf = q0 > llo ? q0 : llo;
+    if ((qf < lhi) && (q0 + V > llo)) {
+      int lo = 0, hi = nload;
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if ((int64_t)ends[mid] > qf) hi = mid;
+        else lo = mid + 1;
+      }
+      int j = lo;
+      uint32_t endj = ends[j];
+      double x = vals[id_map_b[r0 + j]];
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int64_t q = q0 + k;
+        if (q < llo || q >= lhi) continue;
+        if ((uint32_t)q >= endj) {
+          ++j;
+          endj = ends[j];
+          x = vals[id_map_b[r0 + j]];
+        }
+        double y = x;
+        if (WGT) y = __dmul_rn(w[abase + lane * V + k], x);
+        atomicAdd(sums + c[k], y);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <bool WGT>
+__global__ void k_push_exact(int64_t B, const int64_t *__restrict__ row_starts,
+                             const int64_t *__restrict__ edge_starts,
+                             const uint32_t *__restrict__ lro, const uint32_t *__restrict__ id_map,
+                             const uint32_t *__restrict__ col, const double *__restrict__ w,
+                             const double *__restrict__ vals, double *__restrict__ sums,
+                             int64_t only) {
+  const int64_t b = (only >= 0) ? only : (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || (only >= 0 && (blockIdx.x | threadIdx.x))) return;
+  const int64_t rs = row_starts[b], re = row_starts[b + 1], es = edge_starts[b];
+  const uint32_t *lro_b = lro + rs + b;
+  for (int64_t i = 0; i < re - rs; ++i) {
+    const double x = vals[id_map[rs + i]];
+    for (uint32_t e = lro_b[i]; e < lro_b[i + 1]; ++e) {
+      double y = x;
+      if (WGT) y = __dmul_rn(w[es + e], x);
+      const uint32_t d = col[es + e];
+      sums[d] = __dadd_rn(sums[d], y);
+    }
+  }
+}
+
+__global__ void k_add_range(int64_t lo, int64_t hi, const double *__restrict__ local,
+                            double *__restrict__ sums) {
+  for (int64_t v = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < hi;
+       v += (int64_t)gridDim.x * blockDim.x)
+    sums[v] = __dadd_rn(sums[v], local[v]);
+}
+
+// ---------------------------------------------------------------------------
+// drivers
+// ---------------------------------------------------------------------------
+template <typename K, typename... Args>
+static void launch_window(gcb_ctx *ctx, K kernel, unsigned grid, unsigned block, const void *win,
+                          size_t win_bytes, bool use_window, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  if (use_window && win_bytes > 0 && ctx->window_max > 0 && ctx->persist_max > 0) {
+    size_t nb = win_bytes < (size_t)ctx->window_max ? win_bytes : (size_t)ctx->window_max;
+    float ratio = (float)((double)ctx->persist_max / (double)nb);
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = const_cast<void *>(win);
+    attr[0].val.accessPolicyWindow.num_bytes = nb;
+    attr[0].val.accessPolicyWindow.hitRatio = ratio > 1.0f ? 1.0f : ratio;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  GCB_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+  ctx->launches++;
+}
+
+static unsigned tile_grid(gcb_ctx *ctx, int64_t ntiles) {
+  int64_t cap = (int64_t)ctx->num_sms * 8;
+  int64_t g = ceil_div(ntiles, kWarps);
+  if (g > cap) g = cap;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+// per-block pull partials into bg->partials (block_only >= 0 -> one block)
+void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *vals32,
+               bool use_weights, uint32_t flags, int64_t block_only) {
+  ensure_derived(ctx, bg);
+  bg->partials.ensure(bg->L > 0 ? bg->L : 1);
+  const bool exact = flags & GCB_FLAG_EXACT;
+  const bool window = !(flags & GCB_FLAG_NO_L2_WINDOW);
+  const bool wgt = use_weights && bg->weighted;
+  for (int64_t b = 0; b < bg->B; ++b) {
+    if (block_only >= 0 && b != block_only) continue;
+    const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+    if (Lb == 0) continue;
+    const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
+    const uint32_t *lro_b = bg->lro.p + rs + b;
+    double *part_b = bg->partials.p + rs;
+    if (exact || (vals32 == nullptr && vals == nullptr)) {
+      unsigned g = grid_for(Lb, 256, (int64_t)ctx->num_sms * 16);
+      if (wgt)
+        k_pull_exact<true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, bg->w.p + es, lro_b, Lb, vals,
+                                                        part_b);
+      else
+        k_pull_exact<false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, nullptr, lro_b, Lb, vals,
+                                                         part_b);
+      after_launch(ctx, "k_pull_exact");
+      continue;
+    }
+    const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
+    const int64_t t0 = bg->h_tile_t0[b];
+    const int64_t vlo = b * bg->width;
+    const int64_t vhi = (vlo + bg->width < bg->n) ? vlo + bg->width : bg->n;
+    const unsigned g = tile_grid(ctx, nt);
+    const uint32_t *trow = bg->tile_row.p + tb;
+    double *carry_b = bg->carry.p + tb;
+    const double *wp = wgt ? bg->w.p : nullptr;
+    ProfScope ps_gather(ctx, 0);
+    if (vals32) {
+      const void *win = vals32 + vlo;
+      size_t wb = (size_t)(vhi - vlo) * sizeof(float);
+      if (wgt)
+        launch_window(ctx, k_pull_tiles<float, true>, g, kWarps * 32, win, wb, window,
+                      (const uint32_t *)bg->col.p, wp, lro_b, trow, es, ee, t0, nt, (uint32_t)Lb,
+                      vals32, part_b, carry_b);
+      else
+        launch_window(ctx, k_pull_tiles<float, false>, g, kWarps * 32, win, wb, window,
+                      (const uint32_t *)bg->col.p, wp, lro_b, trow, es, ee, t0, nt, (uint32_t)Lb,
+                      vals32, part_b, carry_b);
+    } else {
+      const void *win = vals + vlo;
+      size_t wb = (size_t)(vhi - vlo) * sizeof(double);
+      if (wgt)
+        launch_window(ctx, k_pull_tiles<double, true>, g, kWarps * 32, win, wb, window,
+                      (const uint32_t *)bg->col.p, wp, lro_b, trow, es, ee, t0, nt, (uint32_t)Lb,
+                      vals, part_b, carry_b);
+      else
+        launch_window(ctx, k_pull_tiles<double, false>, g, kWarps * 32, win, wb, window,
+                      (const uint32_t *)bg->col.p, wp, lro_b, trow, es, ee, t0, nt, (uint32_t)Lb,
+                      vals, part_b, carry_b);
+    }
+    const int64_t sb = bg->h_span_base[b], ns = bg->h_span_base[b + 1] - sb;
+    if (ns > 0) {
+      ProfScope ps_fix(ctx, 1);
+      k_fixup<<<grid_for(ns, 128, 4096), 128, 0, ctx->stream>>>(
+          ns, bg->span_tile.p + sb, tb, nt, trow, lro_b, t0, es, carry_b, part_b);
+      after_launch(ctx, "k_fixup");
+    }
+  }
+}
+
+void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out) {
+  ensure_derived(ctx, bg);
+  if (bg->R == 0) return;
+  k_merge<1><<<(unsigned)bg->R, 512, 0, ctx->stream>>>(bg->n, bg->B, bg->R, bg->bounds.p,
+                                                       bg->id_map.p, bg->partials.p, out, nullptr,
+                                                       0.0, 0.0, nullptr, nullptr, nullptr);
+  after_launch(ctx, "k_merge<1>");
+}
+
+void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sums, bool use_weights,
+                  uint32_t flags, int64_t block_only) {
+  ensure_derived(ctx, bg);
+  const bool wgt = use_weights && bg->weighted;
+  if (flags & GCB_FLAG_EXACT) {
+    if (bg->B == 0) return;
+    unsigned g = block_only >= 0 ? 1 : grid_for(bg->B, 64, 1 << 20);
+    unsigned t = block_only >= 0 ? 1 : 64;
+    if (wgt)
+      k_push_exact<true><<<g, t, 0, ctx->stream>>>(bg->B, bg->row_starts.p, bg->edge_starts.p,
+                                                    bg->lro.p, bg->id_map.p, bg->col.p, bg->w.p,
+                                                    vals, sums, block_only);
+    else
+      k_push_exact<false><<<g, t, 0, ctx->stream>>>(bg->B, bg->row_starts.p, bg->edge_starts.p,
+                                                     bg->lro.p, bg->id_map.p, bg->col.p, nullptr,
+                                                     vals, sums, block_only);
+    after_launch(ctx, "k_push_exact");
+    return;
+  }
+  for (int64_t b = 0; b < bg->B; ++b) {
+    if (block_only >= 0 && b != block_only) continue;
+    const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+    if (Lb == 0) continue;
+    const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
+    const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
+    const unsigned g = tile_grid(ctx, nt);
+    if (wgt)
+      k_push_tiles<true><<<g, kWarps * 32, 0, ctx->stream>>>(
+          bg->col.p, bg->w.p, bg->lro.p + rs + b, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
+          (uint32_t)Lb, bg->id_map.p + rs, vals, sums);
+    else
+      k_push_tiles<false><<<g, kWarps * 32, 0, ctx->stream>>>(
+          bg->col.p, nullptr, bg->lro.p + rs + b, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
+          (uint32_t)Lb, bg->id_map.p + rs, vals, sums);
+    after_launch(ctx, "k_push_tiles");
+  }
+}
+
+// PageRank driver shared by pr_blocked / pr_baseline (kernels.py:207-268, 367-405)
+static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, int max_iters,
+                   uint32_t flags, const uint32_t *deg_override, double *ranks_dev, int *iters,
+                   int *conv) {
+  GCB_REQUIRE(damping > 0.0 && damping < 1.0, "damping must lie in (0, 1)");
+  GCB_REQUIRE(tol >= 0.0, "tol must be >= 0");
+  GCB_REQUIRE(max_iters >= 1, "max_iters must be >= 1");
+  GCB_REQUIRE(bg->n > 0, "PageRank needs at least one vertex");
+  ensure_derived(ctx, bg);
+  const int64_t n = bg->n;
+  const bool exact = flags & GCB_FLAG_EXACT;
+  const bool f32 = (flags & GCB_FLAG_F32_VALUES) && !exact && bg->direction == 0;
+  const uint32_t *deg = deg_override ? deg_override : bg->deg.p;
+  bg->contrib.ensure(n);
+  if (f32) bg->contrib32.ensure(n);
+  const bool push = bg->direction == 1;
+  if (push) bg->sums.ensure(n);
+  const unsigned upd_grid = grid_for(n, 256, (int64_t)ctx->num_sms * 8);
+  bg->deltas.ensure((bg->R > (int64_t)upd_grid ? bg->R : (int64_t)upd_grid) + 2);
+  double *delta_dev = bg->deltas.p + bg->deltas.n - 1;
+  const double r0 = 1.0 / (double)n;
+  const double base = (1.0 - damping) / (double)n;
+  k_pr_init<<<grid_for(n, 256, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+      n, r0, deg, ranks_dev, bg->contrib.p, f32 ? bg->contrib32.p : nullptr,
+      push ? bg->sums.p : nullptr);
+  after_launch(ctx, "k_pr_init");
+  double *hdelta = (double *)ctx->pinned;
+  int it = 0, cv = 0;
+  for (int k = 0; k < max_iters; ++k) {
+    int64_t ndeltas;
+    if (!push) {
+      pull_sums(ctx, bg, bg->contrib.p, f32 ? bg->contrib32.p : nullptr, false, flags, -1);
+      if (bg->R > 0) {
+        ProfScope ps(ctx, 2);
+        k_merge<0><<<(unsigned)bg->R, 512, 0, ctx->stream>>>(
+            n, bg->B, bg->R, bg->bounds.p, bg->id_map.p, bg->partials.p, ranks_dev, deg, base,
+            damping, f32 ? nullptr : bg->contrib.p, f32 ? bg->contrib32.p : nullptr,
+            bg->deltas.p);
+        after_launch(ctx, "k_merge<0>");
+      }
+      ndeltas = bg->R;
+    } else {
+      {
+        ProfScope ps(ctx, 0);
+        push_scatter(ctx, bg, bg->contrib.p, bg->sums.p, false, flags, -1);
+      }
+      ProfScope ps(ctx, 2);
+      k_pr_update_push<<<upd_grid, 256, 0, ctx->stream>>>(n, base, damping, bg->sums.p, ranks_dev,
+                                                         deg, bg->contrib.p, bg->deltas.p);
+      after_launch(ctx, "k_pr_update_push");
+      ndeltas = upd_grid;
+    }
+    ++it;
+    if (tol > 0.0) {
+      k_reduce_sum<<<1, 1024, 0, ctx->stream>>>(bg->deltas.p, ndeltas, delta_dev);
+      after_launch(ctx, "k_reduce_sum");
+      d2h(ctx, hdelta, delta_dev, 1);
+      sync(ctx);
+      if (*hdelta < tol) {
+        cv = 1;
+        break;
+      }
+    }
+  }
+  *iters = it;
+  *conv = cv;
+}
+
+}  // namespace gcb
+
+using namespace gcb;
+
+extern "C" {
+
+int gcb_compute_contributions(gcb_ctx *ctx, int64_t n, const double *ranks_host,
+                              const int64_t *out_degrees_host, double *out_host) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && ((ranks_host && out_degrees_host && out_host) || n == 0), "NULL argument");
+  DeviceGuard dg(ctx->device);
+  if (n == 0) return GCB_OK;
+  DArray<double> r(n), o(n);
+  DArray<int64_t> d(n);
+  h2d(ctx, r.p, ranks_host, n);
+  h2d(ctx, d.p, out_degrees_host, n);
+  k_contributions<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, r.p, d.p, o.p);
+  after_launch(ctx, "k_contributions");
+  d2h(ctx, out_host, o.p, n);
+  sync(ctx);
+  GCB_API_END
+}
+
+int gcb_pr_blocked_dev(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, int max_iters,
+                       uint32_t flags, double *ranks_dev, int *iterations, int *converged) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && ranks_dev && iterations && converged, "NULL argument");
+  DeviceGuard dg(ctx->device);
+  pr_run(ctx, bg, damping, tol, max_iters, flags, nullptr, ranks_dev, iterations, converged);
+  GCB_API_END
+}
+
+int gcb_pr_blocked(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, int max_iters,
+                   int64_t k, uint32_t flags, double *ranks_host, int *iterations, int *converged) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && ranks_host && iterations && converged, "NULL argument");
+  GCB_REQUIRE(k >= 1, "range width k must be >= 1");
+  DeviceGuard dg(ctx->device);
+  bg->ranks.ensure(bg->n ? bg->n : 1);
+  pr_run(ctx, bg, damping, tol, max_iters, flags, nullptr, bg->ranks.p, iterations, converged);
+  d2h(ctx, ranks_host, bg->ranks.p, bg->n);
+  sync(ctx);
+  GCB_API_END
+}
+
+static gcb_blocked *compact_for(gcb_ctx *ctx, const gcb_csr *g_const, int direction) {
+  gcb_csr *g = const_cast<gcb_csr *>(g_const);
+  gcb_blocked *v = csr_compact_view(ctx, g);
+  if (v->direction != direction) {
+    // same arena, other degree semantics: rebuild the derived tables
+    v->direction = direction;
+    v->derived = false;
+  }
+  return v;
+}
+
+int gcb_pr_baseline(gcb_ctx *ctx, const gcb_csr *g, int direction, double damping, double tol,
+                    int max_iters, uint32_t flags, const int64_t *out_degrees_host_or_null,
+                    double *ranks_host, int *iterations, int *converged) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && ranks_host && iterations && converged, "NULL argument");
+  GCB_REQUIRE(direction == 0 || direction == 1, "direction must be pull or push");
+  DeviceGuard dg(ctx->device);
+  gcb_blocked *v = compact_for(ctx, g, direction);
+  DArray<uint32_t> dover;
+  if (out_degrees_host_or_null) {
+    std::vector<uint32_t> d32(g->n);
+    for (int64_t i = 0; i < g->n; ++i) {
+      GCB_REQUIRE(out_degrees_host_or_null[i] >= 0 && out_degrees_host_or_null[i] < (int64_t(1) << 32),
+                  "out_degrees out of range");
+      d32[i] = (uint32_t)out_degrees_host_or_null[i];
+    }
+    dover.alloc(g->n);
+    h2d(ctx, dover.p, d32.data(), g->n);
+  }
+  v->ranks.ensure(v->n ? v->n : 1);
+  pr_run(ctx, v, damping, tol, max_iters, flags, out_degrees_host_or_null ? dover.p : nullptr,
+         v->ranks.p, iterations, converged);
+  d2h(ctx, ranks_host, v->ranks.p, v->n);
+  sync(ctx);
+  GCB_API_END
+}
+
+int gcb_process_block_pull(gcb_ctx *ctx, gcb_blocked *bg, int64_t block, const double *contrib_host,
+                           uint32_t flags, double *out_host) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && contrib_host && out_host, "NULL argument");
+  if (block < 0 || block >= bg->B) fail(GCB_EINDEX, "%lld", (long long)block);
+  DeviceGuard dg(ctx->device);
+  ensure_derived(ctx, bg);
+  bg->contrib.ensure(bg->n ? bg->n : 1);
+  h2d(ctx, bg->contrib.p, contrib_host, bg->n);
+  pull_sums(ctx, bg, bg->contrib.p, nullptr, false, flags, block);
+  const int64_t rs = bg->h_row_starts[block], Lb = bg->h_row_starts[block + 1] - rs;
+  d2h(ctx, out_host, bg->partials.p + rs, Lb);
+  sync(ctx);
+  GCB_API_END
+}
+
+int gcb_process_block_push(gcb_ctx *ctx, gcb_blocked *bg, int64_t block, const double *contrib_host,
+                           uint32_t flags, double *sums_host) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && contrib_host && sums_host, "NULL argument");
+  if (block < 0 || block >= bg->B) fail(GCB_EINDEX, "%lld", (long long)block);
+  DeviceGuard dg(ctx->device);
+  ensure_derived(ctx, bg);
+  const int64_t n = bg->n;
+  bg->contrib.ensure(n ? n : 1);
+  bg->sums.ensure(n ? n : 1);
+  DArray<double> local(n ? n : 1), dsums(n ? n : 1);
+  h2d(ctx, bg->contrib.p, contrib_host, n);
+  h2d(ctx, dsums.p, sums_host, n);
+  GCB_CUDA(cudaMemsetAsync(local.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));
+  push_scatter(ctx, bg, bg->contrib.p, local.p, false, flags, block);  // unweighted (kernels.py:291-293)
+  const int64_t lo = block * bg->width, hi = (lo + bg->width < n) ? lo + bg->width : n;
+  if (hi > lo) {
+    k_add_range<<<grid_for(hi - lo, 256, 4096), 256, 0, ctx->stream>>>(lo, hi, local.p, dsums.p);
+    after_launch(ctx, "k_add_range");
+  }
+  d2h(ctx, sums_host, dsums.p, n);
+  sync(ctx);
+  GCB_API_END
+}
+
+int gcb_accumulate_ranges(gcb_ctx *ctx, gcb_blocked *bg, const double *partials_host, int64_t k,
+                          double *out_host) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && out_host && (partials_host || bg->L == 0), "NULL argument");
+  GCB_REQUIRE(k >= 1, "range width k must be >= 1");
+  DeviceGuard dg(ctx->device);
+  ensure_derived(ctx, bg);
+  bg->partials.ensure(bg->L > 0 ? bg->L : 1);
+  h2d(ctx, bg->partials.p, partials_host, bg->L);
+  DArray<double> y(bg->n ? bg->n : 1);
+  merge_to(ctx, bg, y.p);
+  d2h(ctx, out_host, y.p, bg->n);
+  sync(ctx);
+  GCB_API_END
+}
+
+int gcb_segment_row_sums(gcb_ctx *ctx, const gcb_csr *g, const double *values_host, int use_weights,
+                         uint32_t flags, double *out_host) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && out_host && (values_host || g->n == 0), "NULL argument");
+  DeviceGuard dg(ctx->device);
+  gcb_blocked *v = compact_for(ctx, g, 0);
+  DArray<double> x(g->n ? g->n : 1), y(g->n ? g->n : 1);
+  h2d(ctx, x.p, values_host, g->n);
+  pull_sums(ctx, v, x.p, nullptr, use_weights != 0, flags, -1);
+  merge_to(ctx, v, y.p);
+  d2h(ctx, out_host, y.p, g->n);
+  sync(ctx);
+  GCB_API_END
+}
+
+int gcb_spmv(gcb_ctx *ctx, const gcb_csr *g, const double *x_host, int direction, uint32_t flags,
+             double *y_host) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && y_host && (x_host || g->n == 0), "NULL argument");
+  GCB_REQUIRE(direction == 0 || direction == 1, "direction must be pull or push");
+  DeviceGuard dg(ctx->device);
+  gcb_blocked *v = compact_for(ctx, g, direction);
+  DArray<double> x(g->n ? g->n : 1), y(g->n ? g->n : 1);
+  h2d(ctx, x.p, x_host, g->n);
+  if (direction == 0) {
+    pull_sums(ctx, v, x.p, nullptr, true, flags, -1);
+    merge_to(ctx, v, y.p);
+  } else {
+    GCB_CUDA(cudaMemsetAsync(y.p, 0, (g->n ? g->n : 1) * sizeof(double), ctx->stream));
+    push_scatter(ctx, v, x.p, y.p, true, flags, -1);
+  }
+  d2h(ctx, y_host, y.p, g->n);
+  sync(ctx);
+  GCB_API_END
+}
+
+static void spmv_blocked_dev(gcb_ctx *ctx, gcb_blocked *bg, const double *x, uint32_t flags,
+                             double *y) {
+  ensure_derived(ctx, bg);
+  if (bg->direction == 0) {
+    pull_sums(ctx, bg, x, nullptr, true, flags, -1);
+    if (bg->R == 0) return;
+    merge_to(ctx, bg, y);
+  } else {
+    GCB_CUDA(cudaMemsetAsync(y, 0, (bg->n ? bg->n : 1) * sizeof(double), ctx->stream));
+    push_scatter(ctx, bg, x, y, true, flags, -1);
+  }
+}
+
+int gcb_spmv_blocked(gcb_ctx *ctx, gcb_blocked *bg, const double *x_host, int64_t k, uint32_t flags,
+                     double *y_host) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && y_host && (x_host || bg->n == 0), "NULL argument");
+  GCB_REQUIRE(k >= 1, "range width k must be >= 1");
+  DeviceGuard dg(ctx->device);
+  DArray<double> x(bg->n ? bg->n : 1), y(bg->n ? bg->n : 1);
+  h2d(ctx, x.p, x_host, bg->n);
+  spmv_blocked_dev(ctx, bg, x.p, flags, y.p);
+  d2h(ctx, y_host, y.p, bg->n);
+  sync(ctx);
+  GCB_API_END
+}
+
+int gcb_spmv_blocked_dev(gcb_ctx *ctx, gcb_blocked *bg, const double *x_dev, uint32_t flags,
+                         double *y_dev) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && y_dev && (x_dev || bg->n == 0), "NULL argument");
+  DeviceGuard dg(ctx->device);
+  spmv_blocked_dev(ctx, bg, x_dev, flags, y_dev);
+  GCB_API_END
+}
+
+}  // extern "C"

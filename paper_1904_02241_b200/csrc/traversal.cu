@@ -1,0 +1,535 @@
+// traversal.cu -- level-synchronous BFS with the push / blocked-pull direction
+// switch (traversal.py:93-209), frontier SSSP over integer weights, and weakly
+// connected components.
+//
+// Frontier representation: a dense per-vertex flag array for the next level
+// (so the push step needs no atomics and the level queue comes out ascending
+// after a stream compaction, exactly the order np.unique / flatnonzero give in
+// traversal.py:135 and :172) plus a bitmap of the current frontier for the
+// pull step (n/8 bytes: 2 MiB at scale 24, L2-resident).
+#include <algorithm>
+#include <climits>
+
+#include "gcb_internal.cuh"
+
+namespace gcb {
+
+constexpr int32_t kInfDepth = INT32_MAX;
+constexpr int64_t kInfDist = INT64_MAX;
+
+// --------------------------------------------------------------------------
+// BFS push step (forward_push_step traversal.py:121-140): warp per frontier
+// vertex, lanes over out-edges; unvisited destinations get next[v] = 1.
+// --------------------------------------------------------------------------
+__global__ void k_bfs_push(int64_t qsize, const uint32_t *__restrict__ queue,
+                           const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
+                           const int32_t *__restrict__ depth, uint8_t *__restrict__ next) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < qsize; i += nw) {
+    const uint32_t u = queue[i];
+    const int64_t s = ro[u], e = ro[u + 1];
+    for (int64_t k = s + lane; k < e; k += 32) {
+      const uint32_t v = col[k];
+      if (depth[v] == kInfDepth) next[v] = 1;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// BFS blocked pull step (forward_pull_step traversal.py:143-176): per TOCAB
+// block of the transpose, each still-unvisited local row scans its in-range
+// sources against the frontier bitmap.  Depth only, so the row may stop at
+// the first hit (the reference sums the whole row; "sum > 0" == "any").
+// Warp per 32 local rows; lanes cooperate on long rows.
+// --------------------------------------------------------------------------
+__global__ void k_bfs_pull_block(int64_t Lb, const uint32_t *__restrict__ lro_b,
+                                 const uint32_t *__restrict__ id_map_b,
+                                 const uint32_t *__restrict__ col_b,
+                                 const uint32_t *__restrict__ front_bits,
+                                 const int32_t *__restrict__ depth, uint8_t *__restrict__ next) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Lb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = id_map_b[i];
+    if (depth[v] != kInfDepth) continue;
+    const uint32_t e1 = lro_b[i + 1];
+    for (uint32_t e = lro_b[i]; e < e1; ++e) {
+      const uint32_t u = col_b[e];
+      if (front_bits[u >> 5] >> (u & 31) & 1u) {
+        next[v] = 1;
+        break;
+      }
+    }
+  }
+}
+
+// commit level: flags -> ascending queue slice, depth stamp, new bitmap, and
+// the frontier's total out-degree (choose_direction traversal.py:93-99)
+__global__ void k_bfs_commit(int64_t n, int32_t level, uint8_t *__restrict__ next,
+                             const uint32_t *__restrict__ pos, uint32_t *__restrict__ queue_out,
+                             int32_t *__restrict__ depth, uint32_t *__restrict__ front_bits,
+                             const int64_t *__restrict__ ro,
+                             unsigned long long *__restrict__ deg_sum) {
+  __shared__ unsigned long long s_sum;
+  if (threadIdx.x == 0) s_sum = 0;
+  __syncthreads();
+  unsigned long long local = 0;
+  const int64_t nwords = (n + 31) >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nwords * 32;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + threadIdx.x;
+    bool f = false;
+    if (v < n) {
+      f = next[v] != 0;
+      if (f) {
+        queue_out[pos[v]] = (uint32_t)v;
+        depth[v] = level;
+        next[v] = 0;
+        local += (unsigned long long)(ro[v + 1] - ro[v]);
+      }
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && (v >> 5) < nwords) front_bits[v >> 5] = word;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xffffffffu, local, d);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_sum, local);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(deg_sum, s_sum);
+}
+
+__global__ void k_flags_u32(int64_t n, const uint8_t *__restrict__ next, uint32_t *__restrict__ f) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    f[v] = next[v];
+}
+
+static gcb_blocked *default_pull_blocking(gcb_ctx *ctx, const gcb_csr *g,
+                                          gcb_blocked **owned) {
+  // traversal.py:186-187: partition_tocab(transpose(g), "pull", max(1, n // 8))
+  gcb_csr *gt = nullptr;
+  int rc = gcb_csr_transpose(ctx, g, &gt);
+  if (rc != GCB_OK) fail(rc, "%s", gcb_last_error());
+  try {
+    *owned = partition_device(ctx, gt, 0, std::max<int64_t>(1, g->n / 8));
+  } catch (...) {
+    gcb_csr_destroy(gt);
+    throw;
+  }
+  gcb_csr_destroy(gt);
+  return *owned;
+}
+
+struct Frontier {
+  DArray<uint8_t> next;
+  DArray<uint32_t> flags, pos, bits;
+  DArray<unsigned long long> degsum;
+  explicit Frontier(int64_t n) {
+    next.alloc(n ? n : 1);
+    flags.alloc(n + 1);
+    pos.alloc(n + 1);
+    bits.alloc((n + 31) / 32 + 1);
+    degsum.alloc(1);
+  }
+};
+
+// flags -> queue slice at `out`; returns (count, degree sum) after a sync
+static void commit_level(gcb_ctx *ctx, const gcb_csr *g, Frontier &F, int32_t level,
+                         uint32_t *out, int32_t *depth, int64_t *count, uint64_t *degsum) {
+  const int64_t n = g->n;
+  k_flags_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, F.next.p, F.flags.p);
+  after_launch(ctx, "k_flags_u32");
+  GCB_CUDA(cudaMemsetAsync(F.flags.p + n, 0, sizeof(uint32_t), ctx->stream));
+  cub_exclusive_sum_u32(ctx, F.flags.p, F.pos.p, n + 1);
+  GCB_CUDA(cudaMemsetAsync(F.degsum.p, 0, sizeof(unsigned long long), ctx->stream));
+  k_bfs_commit<<<grid_for(((n + 31) / 32) * 32, 256, (int64_t)ctx->num_sms * 8), 256, 0,
+                 ctx->stream>>>(n, level, F.next.p, F.pos.p, out, depth, F.bits.p, g->ro.p,
+                                F.degsum.p);
+  after_launch(ctx, "k_bfs_commit");
+  uint32_t *h = (uint32_t *)ctx->pinned;
+  unsigned long long *hs = (unsigned long long *)((char *)ctx->pinned + 64);
+  d2h(ctx, h, F.pos.p + n, 1);
+  d2h(ctx, hs, F.degsum.p, 1);
+  sync(ctx);
+  *count = *h;
+  *degsum = *hs;
+}
+
+__global__ void k_fill_i32(int64_t n, int32_t v, int32_t *p) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_fill_i64(int64_t n, int64_t v, int64_t *p) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_seed(int64_t src, int32_t *depth, uint32_t *queue, uint32_t *bits) {
+  depth[src] = 0;
+  queue[0] = (uint32_t)src;
+  bits[src >> 5] = 1u << (src & 31);
+}
+
+static void bfs_run(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int64_t source, int mode,
+                    int64_t capacity, int64_t value_bytes, int32_t *depth_dev, uint32_t *levels_dev,
+                    std::vector<int64_t> &level_sizes, std::vector<uint8_t> &dirs) {
+  const int64_t n = g->n;
+  Frontier F(n);
+  k_fill_i32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, kInfDepth, depth_dev);
+  after_launch(ctx, "k_fill_i32");
+  GCB_CUDA(cudaMemsetAsync(F.next.p, 0, n, ctx->stream));
+  GCB_CUDA(cudaMemsetAsync(F.bits.p, 0, ((n + 31) / 32 + 1) * sizeof(uint32_t), ctx->stream));
+  k_seed<<<1, 1, 0, ctx->stream>>>(source, depth_dev, levels_dev, F.bits.p);
+  after_launch(ctx, "k_seed");
+  int64_t qoff = 0, qsize = 1;
+  uint64_t work = (uint64_t)0;
+  {
+    int64_t h[2];
+    d2h(ctx, &h[0], g->ro.p + source, 2);
+    sync(ctx);
+    work = (uint64_t)(h[1] - h[0]);
+  }
+  level_sizes.push_back(1);
+  int32_t level = 0;
+  while (qsize > 0) {
+    bool pull;
+    if (mode == GCB_BFS_FORCE_PUSH) pull = false;
+    else if (mode == GCB_BFS_FORCE_PULL) pull = true;
+    else pull = (unsigned __int128)work * (unsigned __int128)value_bytes > (unsigned __int128)capacity;
+    dirs.push_back(pull ? 1 : 0);
+    if (!pull) {
+      k_bfs_push<<<grid_for(qsize * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          qsize, levels_dev + qoff, g->ro.p, g->col.p, depth_dev, F.next.p);
+      after_launch(ctx, "k_bfs_push");
+    } else {
+      for (int64_t b = 0; b < bg->B; ++b) {
+        const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+        if (!Lb) continue;
+        const int64_t es = bg->h_edge_starts[b];
+        k_bfs_pull_block<<<grid_for(Lb, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+            Lb, bg->lro.p + rs + b, bg->id_map.p + rs, bg->col.p + es, F.bits.p, depth_dev,
+            F.next.p);
+        after_launch(ctx, "k_bfs_pull_block");
+      }
+    }
+    int64_t cnt = 0;
+    uint64_t ds = 0;
+    commit_level(ctx, g, F, level + 1, levels_dev + qoff + qsize, depth_dev, &cnt, &ds);
+    qoff += qsize;
+    qsize = cnt;
+    work = ds;
+    level += 1;
+    if (qsize) level_sizes.push_back(qsize);
+  }
+}
+
+// --------------------------------------------------------------------------
+// SSSP (integer weights): frontier Bellman-Ford.  A round relaxes the out-
+// edges of every vertex whose distance dropped in the previous round, either
+// pushing with 64-bit atomicMin or pulling over the TOCAB blocks of the
+// transpose (min over frontier in-neighbours).  The fixpoint is the unique
+// shortest-distance vector, independent of direction and relaxation order.
+// --------------------------------------------------------------------------
+__global__ void k_sssp_push(int64_t qsize, const uint32_t *__restrict__ queue,
+                            const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
+                            const double *__restrict__ w, long long *__restrict__ dist,
+                            uint8_t *__restrict__ next) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < qsize; i += nw) {
+    const uint32_t u = queue[i];
+    const long long du = dist[u];
+    const int64_t s = ro[u], e = ro[u + 1];
+    for (int64_t k = s + lane; k < e; k += 32) {
+      const uint32_t v = col[k];
+      const long long nd = du + (long long)w[k];
+      if (nd < dist[v]) {
+        const long long old = atomicMin(&dist[v], nd);
+        if (nd < old) next[v] = 1;
+      }
+    }
+  }
+}
+
+__global__ void k_sssp_pull_block(int64_t Lb, const uint32_t *__restrict__ lro_b,
+                                  const uint32_t *__restrict__ id_map_b,
+                                  const uint32_t *__restrict__ col_b, const double *__restrict__ w_b,
+                                  const uint32_t *__restrict__ front_bits,
+                                  long long *__restrict__ dist, uint8_t *__restrict__ next) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Lb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = id_map_b[i];
+    long long best = dist[v];
+    const long long before = best;
+    const uint32_t e1 = lro_b[i + 1];
+    for (uint32_t e = lro_b[i]; e < e1; ++e) {
+      const uint32_t u = col_b[e];
+      if (front_bits[u >> 5] >> (u & 31) & 1u) {
+        const long long du = dist[u];
+        if (du != LLONG_MAX) {
+          const long long cand = du + (long long)w_b[e];
+          if (cand < best) best = cand;
+        }
+      }
+    }
+    if (best < before) {
+      const long long old = atomicMin(&dist[v], best);
+      if (best < old) next[v] = 1;
+    }
+  }
+}
+
+// commit round: flags -> queue, bitmap; returns count + frontier out-degree
+__global__ void k_sssp_commit(int64_t n, uint8_t *__restrict__ next, const uint32_t *__restrict__ pos,
+                              uint32_t *__restrict__ queue_out, uint32_t *__restrict__ front_bits,
+                              const int64_t *__restrict__ ro,
+                              unsigned long long *__restrict__ deg_sum) {
+  __shared__ unsigned long long s_sum;
+  if (threadIdx.x == 0) s_sum = 0;
+  __syncthreads();
+  unsigned long long local = 0;
+  const int64_t nwords = (n + 31) >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nwords * 32;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + threadIdx.x;
+    bool f = false;
+    if (v < n) {
+      f = next[v] != 0;
+      if (f) {
+        queue_out[pos[v]] = (uint32_t)v;
+        next[v] = 0;
+        local += (unsigned long long)(ro[v + 1] - ro[v]);
+      }
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && (v >> 5) < nwords) front_bits[v >> 5] = word;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xffffffffu, local, d);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_sum, local);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(deg_sum, s_sum);
+}
+
+// --------------------------------------------------------------------------
+// CC: lock-free union-find, always hooking the larger root under the smaller
+// one, so every final root is its component's minimum vertex id.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t uf_find(uint32_t *parent, uint32_t x) {
+  while (true) {
+    const uint32_t p = __ldcg(parent + x);
+    if (p == x) return x;
+    const uint32_t gp = __ldcg(parent + p);
+    if (gp != p) parent[x] = gp;  // path halving (benign race: gp <= p < x)
+    x = p;
+  }
+}
+
+__global__ void k_cc_init(int64_t n, uint32_t *parent) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    parent[v] = (uint32_t)v;
+}
+
+__global__ void k_cc_hook(int64_t n, const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
+                          uint32_t *parent) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp; u < n; u += nw) {
+    const int64_t s = ro[u], e = ro[u + 1];
+    for (int64_t k = s + lane; k < e; k += 32) {
+      uint32_t a = (uint32_t)u, b = col[k];
+      while (true) {
+        a = uf_find(parent, a);
+        b = uf_find(parent, b);
+        if (a == b) break;
+        const uint32_t hi = a > b ? a : b, lo = a > b ? b : a;
+        const uint32_t old = atomicCAS(&parent[hi], hi, lo);
+        if (old == hi) break;
+        a = old;  // hi got a new parent; retry from it
+        b = lo;
+      }
+    }
+  }
+}
+
+__global__ void k_cc_compress(int64_t n, uint32_t *parent, unsigned long long *count) {
+  unsigned long long local = 0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)v;
+    while (parent[x] != x) x = parent[x];
+    parent[v] = x;
+    local += (x == (uint32_t)v);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xffffffffu, local, d);
+  if ((threadIdx.x & 31) == 0) atomicAdd(count, local);
+}
+
+}  // namespace gcb
+
+using namespace gcb;
+
+extern "C" {
+
+int gcb_bfs(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t source, int mode,
+            int64_t capacity_bytes, int64_t value_bytes, int32_t *depth_host,
+            uint32_t *level_verts_host, int64_t *level_sizes_host, uint8_t *directions_host,
+            int64_t max_levels, int64_t *num_levels, int64_t *num_expansions) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && depth_host && num_levels && num_expansions, "NULL argument");
+  GCB_REQUIRE(source >= 0 && source < g->n, "source %lld out of range", (long long)source);
+  GCB_REQUIRE(mode >= 0 && mode <= 2, "unknown direction mode");
+  GCB_REQUIRE(capacity_bytes >= 1 && value_bytes >= 1, "capacity and value size must be positive");
+  DeviceGuard dg(ctx->device);
+  gcb_blocked *owned = nullptr;
+  gcb_blocked *bg = bg_pull;
+  if (mode != GCB_BFS_FORCE_PUSH && !bg) bg = default_pull_blocking(ctx, g, &owned);
+  try {
+    if (bg) {
+      GCB_REQUIRE(bg->n == g->n && bg->direction == 0, "g_blocked must be a pull blocking of g");
+      ensure_derived(ctx, bg);
+    }
+    DArray<int32_t> depth(g->n ? g->n : 1);
+    DArray<uint32_t> levels(g->n ? g->n : 1);
+    std::vector<int64_t> sizes;
+    std::vector<uint8_t> dirs;
+    bfs_run(ctx, g, bg, source, mode, capacity_bytes, value_bytes, depth.p, levels.p, sizes, dirs);
+    int64_t total = 0;
+    for (auto s : sizes) total += s;
+    d2h(ctx, depth_host, depth.p, g->n);
+    if (level_verts_host) d2h(ctx, level_verts_host, levels.p, total);
+    sync(ctx);
+    *num_levels = (int64_t)sizes.size();
+    *num_expansions = (int64_t)dirs.size();
+    for (int64_t i = 0; i < (int64_t)sizes.size() && i < max_levels; ++i) {
+      if (level_sizes_host) level_sizes_host[i] = sizes[i];
+    }
+    for (int64_t i = 0; i < (int64_t)dirs.size() && i < max_levels; ++i)
+      if (directions_host) directions_host[i] = dirs[i];
+  } catch (...) {
+    if (owned) gcb_blocked_destroy(owned);
+    throw;
+  }
+  if (owned) gcb_blocked_destroy(owned);
+  GCB_API_END
+}
+
+int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t source, int mode,
+             int64_t capacity_bytes, int64_t value_bytes, int64_t *dist_host,
+             uint8_t *directions_host, int64_t max_rounds, int64_t *rounds) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && dist_host && rounds, "NULL argument");
+  GCB_REQUIRE(g->weighted, "SSSP needs integer edge weights on the graph");
+  GCB_REQUIRE(source >= 0 && source < g->n, "source %lld out of range", (long long)source);
+  GCB_REQUIRE(mode >= 0 && mode <= 2, "unknown direction mode");
+  DeviceGuard dg(ctx->device);
+  gcb_blocked *bg = bg_pull;
+  if (mode == GCB_BFS_FORCE_PULL) GCB_REQUIRE(bg, "force-pull SSSP needs a weighted pull blocking");
+  if (bg) {
+    GCB_REQUIRE(bg->n == g->n && bg->direction == 0 && bg->weighted,
+                "g_blocked must be a weighted pull blocking of g");
+    ensure_derived(ctx, bg);
+  }
+  const int64_t n = g->n;
+  DArray<int64_t> dist(n ? n : 1);
+  DArray<uint32_t> queue(n ? n : 1);
+  Frontier F(n);
+  k_fill_i64<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, kInfDist, dist.p);
+  after_launch(ctx, "k_fill_i64");
+  GCB_CUDA(cudaMemsetAsync(F.next.p, 0, n, ctx->stream));
+  GCB_CUDA(cudaMemsetAsync(F.bits.p, 0, ((n + 31) / 32 + 1) * sizeof(uint32_t), ctx->stream));
+  {
+    int64_t zero = 0;
+    uint32_t s32 = (uint32_t)source, bit = 1u << (source & 31);
+    h2d(ctx, dist.p + source, &zero, 1);
+    h2d(ctx, queue.p, &s32, 1);
+    h2d(ctx, F.bits.p + (source >> 5), &bit, 1);
+    sync(ctx);
+  }
+  int64_t qsize = 1, r = 0;
+  uint64_t work;
+  {
+    int64_t h[2];
+    d2h(ctx, &h[0], g->ro.p + source, 2);
+    sync(ctx);
+    work = (uint64_t)(h[1] - h[0]);
+  }
+  while (qsize > 0) {
+    bool pull;
+    if (mode == GCB_BFS_FORCE_PUSH || !bg) pull = false;
+    else if (mode == GCB_BFS_FORCE_PULL) pull = true;
+    else pull = (unsigned __int128)work * (unsigned __int128)value_bytes > (unsigned __int128)capacity_bytes;
+    if (directions_host && r < max_rounds) directions_host[r] = pull ? 1 : 0;
+    if (!pull) {
+      k_sssp_push<<<grid_for(qsize * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          qsize, queue.p, g->ro.p, g->col.p, g->w.p, (long long *)dist.p, F.next.p);
+      after_launch(ctx, "k_sssp_push");
+    } else {
+      for (int64_t b = 0; b < bg->B; ++b) {
+        const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+        if (!Lb) continue;
+        const int64_t es = bg->h_edge_starts[b];
+        k_sssp_pull_block<<<grid_for(Lb, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+            Lb, bg->lro.p + rs + b, bg->id_map.p + rs, bg->col.p + es, bg->w.p + es, F.bits.p,
+            (long long *)dist.p, F.next.p);
+        after_launch(ctx, "k_sssp_pull_block");
+      }
+    }
+    // compact next flags into the queue
+    k_flags_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, F.next.p, F.flags.p);
+    after_launch(ctx, "k_flags_u32");
+    GCB_CUDA(cudaMemsetAsync(F.flags.p + n, 0, sizeof(uint32_t), ctx->stream));
+    cub_exclusive_sum_u32(ctx, F.flags.p, F.pos.p, n + 1);
+    GCB_CUDA(cudaMemsetAsync(F.degsum.p, 0, sizeof(unsigned long long), ctx->stream));
+    k_sssp_commit<<<grid_for(((n + 31) / 32) * 32, 256, (int64_t)ctx->num_sms * 8), 256, 0,
+                    ctx->stream>>>(n, F.next.p, F.pos.p, queue.p, F.bits.p, g->ro.p, F.degsum.p);
+    after_launch(ctx, "k_sssp_commit");
+    uint32_t *h = (uint32_t *)ctx->pinned;
+    unsigned long long *hs = (unsigned long long *)((char *)ctx->pinned + 64);
+    d2h(ctx, h, F.pos.p + n, 1);
+    d2h(ctx, hs, F.degsum.p, 1);
+    sync(ctx);
+    qsize = *h;
+    work = *hs;
+    ++r;
+  }
+  d2h(ctx, dist_host, dist.p, n);
+  sync(ctx);
+  *rounds = r;
+  GCB_API_END
+}
+
+int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_components) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && labels_host, "NULL argument");
+  DeviceGuard dg(ctx->device);
+  const int64_t n = g->n;
+  DArray<uint32_t> parent(n ? n : 1);
+  DArray<unsigned long long> cnt(1);
+  GCB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
+  k_cc_init<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, parent.p);
+  after_launch(ctx, "k_cc_init");
+  if (g->m) {
+    k_cc_hook<<<grid_for(n * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        n, g->ro.p, g->col.p, parent.p);
+    after_launch(ctx, "k_cc_hook");
+  }
+  k_cc_compress<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, parent.p, cnt.p);
+  after_launch(ctx, "k_cc_compress");
+  unsigned long long hc = 0;
+  d2h(ctx, labels_host, parent.p, n);
+  d2h(ctx, &hc, cnt.p, 1);
+  sync(ctx);
+  if (num_components) *num_components = (int64_t)hc;
+  GCB_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,176 @@
+"""Level-synchronous traversal with the push / blocked-pull switch
+(mirrors gcb.traversal, traversal.py:1-287) plus integer-weight SSSP.
+
+``bfs`` runs entirely on the B200: push steps expand the frontier queue,
+pull steps scan the TOCAB blocks of the transpose against a frontier bitmap,
+and the per-level choice is choose_direction's rule (traversal.py:93-99)
+evaluated on a device reduction of the frontier's out-degrees.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+import numpy as np
+
+from . import _lib
+from .blocking import BlockedGraph, partition_tocab
+from .graph import CsrGraph, transpose
+
+__all__ = [
+    "INF_DEPTH",
+    "INF_DIST",
+    "DirectionPolicy",
+    "TraversalState",
+    "BfsResult",
+    "SsspResult",
+    "choose_direction",
+    "bfs",
+    "sssp",
+    "sample_sources",
+]
+
+INF_DEPTH = np.iinfo(np.int32).max  # traversal.py:43
+INF_DIST = np.iinfo(np.int64).max
+
+
+@dataclasses.dataclass(frozen=True)
+class DirectionPolicy:
+    """Pull when the frontier's out-degree sum times value_bytes exceeds the
+    cache capacity (traversal.py:46-61)."""
+
+    mode: str = "auto"
+    cache_capacity_bytes: int = 2_883_584
+    value_bytes: int = 4
+
+    MODES = ("auto", "force-push", "force-pull")
+
+    def __post_init__(self):
+        if self.mode not in self.MODES:
+            raise ValueError(f"unknown direction mode {self.mode!r}")
+        if self.cache_capacity_bytes < 1 or self.value_bytes < 1:
+            raise ValueError("capacity and value size must be positive")
+
+    @property
+    def code(self) -> int:
+        return {"auto": _lib.BFS_AUTO, "force-push": _lib.BFS_FORCE_PUSH,
+                "force-pull": _lib.BFS_FORCE_PULL}[self.mode]
+
+
+@dataclasses.dataclass
+class TraversalState:
+    depth: np.ndarray
+    sigma: np.ndarray
+    frontier: np.ndarray
+    level: int = 0
+
+    @classmethod
+    def initial(cls, n: int, source: int) -> "TraversalState":
+        depth = np.full(n, INF_DEPTH, dtype=np.int32)
+        sigma = np.zeros(n, dtype=np.float64)
+        depth[source] = 0
+        sigma[source] = 1.0
+        return cls(depth, sigma, np.array([source], dtype=np.uint32))
+
+
+@dataclasses.dataclass
+class BfsResult:
+    depth: np.ndarray
+    levels: list
+    directions: list
+
+
+@dataclasses.dataclass
+class SsspResult:
+    dist: np.ndarray  # int64, INF_DIST = unreachable
+    rounds: int
+    directions: list
+
+
+def choose_direction(g: CsrGraph, state: TraversalState, policy: DirectionPolicy) -> str:
+    """traversal.py:93-99 (strictly-greater switch)."""
+    if policy.mode == "force-push":
+        return "push"
+    if policy.mode == "force-pull":
+        return "blocked-pull"
+    working_set = int(g.out_degrees[state.frontier].sum()) * policy.value_bytes
+    return "blocked-pull" if working_set > policy.cache_capacity_bytes else "push"
+
+
+def _check_source(g: CsrGraph, source: int):
+    if not 0 <= int(source) < g.num_vertices:
+        raise ValueError(f"source {source} out of range")
+
+
+def bfs(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
+        policy: DirectionPolicy = DirectionPolicy()) -> BfsResult:
+    """Level-synchronous BFS (traversal.py:201-209); INF_DEPTH = unreached.
+    Without ``g_blocked`` the pull side uses partition_tocab(transpose(g),
+    "pull", max(1, n // 8)) as the reference does (traversal.py:186-187)."""
+    _check_source(g, source)
+    n = g.num_vertices
+    h = g.device()
+    bgh = None
+    if policy.mode != "force-push":
+        if g_blocked is None:
+            g_blocked = partition_tocab(transpose(g), "pull", max(1, n // 8))
+        bgh = g_blocked.device()
+    depth = np.empty(n, dtype=np.int32)
+    verts = np.empty(n, dtype=np.uint32)
+    cap = n + 2
+    sizes = np.zeros(cap, dtype=np.int64)
+    dirs = np.zeros(cap, dtype=np.uint8)
+    nl, ne = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(h.ctx._lib.gcb_bfs(
+        h.ctx.handle, h.raw, None if bgh is None else bgh.raw, int(source), policy.code,
+        int(policy.cache_capacity_bytes), int(policy.value_bytes), _lib.ptr(depth, _lib.P_i32),
+        _lib.ptr(verts, _lib.P_u32), _lib.ptr(sizes, _lib.P_i64), _lib.ptr(dirs, _lib.P_u8), cap,
+        ctypes.byref(nl), ctypes.byref(ne)), "bfs")
+    bounds = np.concatenate([[0], np.cumsum(sizes[: nl.value])])
+    levels = [verts[bounds[i]:bounds[i + 1]].copy() for i in range(nl.value)]
+    directions = ["blocked-pull" if d else "push" for d in dirs[: ne.value]]
+    return BfsResult(depth, levels, directions)
+
+
+def sssp(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
+         policy: DirectionPolicy = DirectionPolicy(value_bytes=8)) -> SsspResult:
+    """Single-source shortest paths over non-negative integer edge weights.
+
+    Not in the reference (SPEC.md:381 lists SSSP as a non-goal); named by the
+    north star.  ``g`` must carry integral float64 weights (< 2^53).  Frontier
+    Bellman-Ford; each round pushes (64-bit atomicMin) or pulls over the TOCAB
+    blocks of the weighted transpose by choose_direction's rule.  Parallel
+    edges act as their minimum weight."""
+    _check_source(g, source)
+    if not g.weighted:
+        raise ValueError("sssp needs integer edge weights on the graph")
+    n = g.num_vertices
+    h = g.device()
+    bgh = None
+    if policy.mode != "force-push":
+        if g_blocked is None:
+            g_blocked = partition_tocab(transpose(g), "pull", max(1, n // 8))
+        if not g_blocked.weighted:
+            raise ValueError("g_blocked must carry the edge weights")
+        bgh = g_blocked.device()
+    dist = np.empty(n, dtype=np.int64)
+    cap = 1 << 16
+    dirs = np.zeros(cap, dtype=np.uint8)
+    rounds = ctypes.c_int64()
+    _lib.check(h.ctx._lib.gcb_sssp(h.ctx.handle, h.raw, None if bgh is None else bgh.raw,
+                                   int(source), policy.code, int(policy.cache_capacity_bytes),
+                                   int(policy.value_bytes), _lib.ptr(dist, _lib.P_i64),
+                                   _lib.ptr(dirs, _lib.P_u8), cap, ctypes.byref(rounds)), "sssp")
+    r = rounds.value
+    directions = ["blocked-pull" if d else "push" for d in dirs[: min(r, cap)]]
+    return SsspResult(dist, r, directions)
+
+
+def sample_sources(g: CsrGraph, count: int, seed: int = 12345) -> np.ndarray:
+    """Deterministic uniform source sample (traversal.py:281-287)."""
+    rng = np.random.default_rng(seed)
+    n = g.num_vertices
+    if count >= n:
+        return np.arange(n, dtype=np.int64)
+    return np.sort(rng.choice(n, size=count, replace=False)).astype(np.int64)
