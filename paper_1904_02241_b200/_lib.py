@@ -86,7 +86,7 @@ SIGNATURES = {
 }
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 
 
 class GcbError(RuntimeError):

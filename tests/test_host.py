@@ -43,6 +43,23 @@ class TestLibrary:
         lib = _lib.load()
         assert lib.gcb_version() >= 10000
 
+    def test_context_fails_loudly_without_gpu(self):
+        import subprocess
+        import sys
+
+        code = ("import paper_1904_02241_b200._lib as L\n"
+                "try:\n    L.context()\nexcept Exception as e:\n    print(type(e).__name__)\n"
+                "else:\n    print('OK')\n")
+        out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True,
+                             text=True, timeout=120)
+        got = out.stdout.strip()
+        import torch
+
+        if torch.cuda.is_available():
+            assert got == "OK"
+        else:
+            assert got in ("GcbError", "ValueError"), out
+
     def test_errors_map_without_device(self):
         lib = _lib.load()
         with pytest.raises(ValueError):
