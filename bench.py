@@ -45,8 +45,10 @@ def parse_args():
     p.add_argument("--edge-factor", type=int, default=16)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--iters", type=int, default=10)
-    p.add_argument("--width", type=int, default=1 << 22,
-                   help="TOCAB block width (2^22: 32 MiB f64 value slices, 1/4 of L2)")
+    p.add_argument("--width", type=int, default=0,
+                   help="TOCAB block width; 0 = the largest power of two whose f64 value "
+                        "slice fits in 55%% of the device L2 (2^23 on B200: two 64 MiB blocks "
+                        "at scale 24)")
     p.add_argument("--direction", choices=("pull", "push"), default="pull")
     p.add_argument("--f32-values", action="store_true")
     p.add_argument("--exact", action="store_true")
@@ -216,7 +218,9 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = _lib.context(local)
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy) stream shared by the library and the timing events
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
     # ---- setup (untimed): device R-MAT -> transpose -> TOCAB partition ----
@@ -397,8 +401,28 @@ def run_e2e(args, bg, ctx, stream, flags, steps=None):
                     "gcb_pr_blocked (ranks to host)"}
 
 
+def auto_width(args) -> int:
+    """TOCAB sizing rule (north star (1)): one block's f64 value slice must fit
+    in L2 next to the streamed arenas -> <= 55% of the L2 the device reports."""
+    l2 = 126 * 2 ** 20
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            l2 = int(torch.cuda.get_device_properties(0).L2_cache_size)
+    except Exception:
+        pass
+    budget = int(l2 * 0.55) // 8
+    w = 1
+    while w * 2 <= budget and w < (1 << args.scale):
+        w *= 2
+    return w
+
+
 def main():
     args = parse_args()
+    if args.width <= 0:
+        args.width = auto_width(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -55,6 +55,19 @@ void cub_sort_pairs_u32_u32(gcb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, ui
   *res_vals = dv.Current();
 }
 
+void cub_sort_pairs_desc_u32_u32(gcb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
+                                 uint32_t *vals_alt, int64_t m, uint32_t **res_keys,
+                                 uint32_t **res_vals) {
+  cub::DoubleBuffer<uint32_t> dk(keys, keys_alt);
+  cub::DoubleBuffer<uint32_t> dv(vals, vals_alt);
+  if (m > 0)
+    run_cub(ctx, [&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortPairsDescending(t, b, dk, dv, m, 0, 32, ctx->stream);
+    });
+  *res_keys = dk.Current();
+  *res_vals = dv.Current();
+}
+
 void cub_exclusive_sum_u32(gcb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t count) {
   if (count <= 0) return;
   run_cub(ctx, [&](void *t, size_t &b) {

@@ -152,9 +152,17 @@ struct gcb_blocked {
   std::vector<int64_t> h_tile_base;  // [B+1] prefix of tiles per block
   gcb::DArray<uint32_t> tile_row;    // per tile: local row of first valid edge
   std::vector<int64_t> h_span_base;  // [B+1] prefix of carry-span starts
-  gcb::DArray<uint32_t> span_tile;   // tile ids (block-local) starting a carry span
+  gcb::DArray<uint32_t> span_tile;   // tile ids (global) of each row's first carry tile
+  gcb::DArray<uint32_t> span_len;    // number of consecutive carry tiles of that row
   int64_t R = 0;                     // merge ranges (ceil(n / kMergeK))
   gcb::DArray<int64_t> bounds;       // [B][R+1] arena positions per range
+
+  // ---- execution layout of the fast accumulate gather (ensure_exec) ----
+  bool xready = false;
+  int64_t hot_k = 0;                 // hot slots per block (0: staging disabled)
+  gcb::DArray<uint32_t> xcol;        // col arena recoded: 0x80000000|slot for hot sources
+  gcb::DArray<uint32_t> hot_ids;     // [B][hot_k] source id of each slot (or ~0u)
+  gcb::DArray<double> hotval;        // [B][hot_k] staged values for the next gather
 
   // ---- workspaces (grown on demand) ----
   gcb::DArray<double> partials;  // [L]
@@ -247,8 +255,15 @@ gcb_blocked *csr_compact_view(gcb_ctx *ctx, gcb_csr *g);
 void compute_range_bounds(gcb_ctx *ctx, const gcb_blocked *bg, int64_t k, int64_t *bounds_dev);
 // value kernels (pr.cu)
 void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *vals32,
-               bool use_weights, uint32_t flags, int64_t block_only);
+               bool use_weights, uint32_t flags, int64_t block_only, double *out, bool accum);
 void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out);
+// gather.cu: fast pull gather accumulating into a dense vector (hot staging)
+void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg);
+void gather_accum(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights,
+                  uint32_t flags, double *out);
+void cub_sort_pairs_desc_u32_u32(gcb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
+                                 uint32_t *vals_alt, int64_t m, uint32_t **res_keys,
+                                 uint32_t **res_vals);
 void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sums,
                   bool use_weights, uint32_t flags, int64_t block_only);
 // cub wrappers (cub_ops.cu)

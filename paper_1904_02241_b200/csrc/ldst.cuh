@@ -1,0 +1,47 @@
+// ldst.cuh -- cache-hinted global loads shared by the gather kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace gcb {
+
+// ---------------------------------------------------------------------------
+// cache-policy loads (createpolicy: evict_first for streams read once,
+// evict_last for the per-block vertex-value slice)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const void *ptr, uint64_t pol) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream_d2(const void *ptr, uint64_t pol) {
+  double2 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+      : "=d"(r.x), "=d"(r.y)
+      : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
+  double r;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_keep(const float *p, uint64_t pol) {
+  float r;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return (double)r;
+}
+
+}  // namespace gcb

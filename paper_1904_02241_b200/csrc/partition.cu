@@ -242,6 +242,20 @@ __global__ void k_compact_spans(int64_t ntiles, const uint32_t *__restrict__ sta
     if (start[t]) out[pos[t]] = (uint32_t)t;
 }
 
+// length of each carry span: consecutive carry tiles continuing the same row
+__global__ void k_span_len(int64_t nspans, int64_t ntiles, const uint32_t *__restrict__ span_tile,
+                           const uint32_t *__restrict__ tile_row, const uint32_t *__restrict__ cflag,
+                           uint32_t *__restrict__ len) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nspans;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = span_tile[s];
+    const uint32_t r = tile_row[t];
+    int64_t tt = t;
+    while (tt < ntiles && cflag[tt] && tile_row[tt] == r) ++tt;
+    len[s] = (uint32_t)(tt - t);
+  }
+}
+
 // bounds[b][j] = row_starts[b] + lower_bound(id_map_b, j*k), j in [0, R]
 __global__ void k_range_bounds(int64_t B, int64_t R, int64_t k, const int64_t *__restrict__ row_starts,
                                const uint32_t *__restrict__ id_map, int64_t *__restrict__ bounds) {
@@ -336,6 +350,12 @@ void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
     k_compact_spans<<<grid_for(T, 256, 65536), 256, 0, ctx->stream>>>(T, sflag.p, spos.p,
                                                                       bg->span_tile.p);
     after_launch(ctx, "k_compact_spans");
+    bg->span_len.alloc(nspans);
+    if (nspans) {
+      k_span_len<<<grid_for(nspans, 256, 65536), 256, 0, ctx->stream>>>(
+          nspans, T, bg->span_tile.p, bg->tile_row.p, cflag.p, bg->span_len.p);
+      after_launch(ctx, "k_span_len");
+    }
     for (int64_t b = 0; b <= B; ++b) bg->h_span_base[b] = hpos[b];
   }
   // span tile ids were global; kernels subtract the block's tile base

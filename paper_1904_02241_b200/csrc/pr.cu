@@ -1,14 +1,23 @@
 // pr.cu -- TOCAB value kernels on sm_100a and their drivers:
 //   K2 pull gather  (kernels.py:155-161, 275-282, 333-347)
-//   K3 range-tiled merge fused with the rank update / contributions / delta
-//      (kernels.py:300-321, 185-191, 398-399)
+//   K3 block merge  (accumulate_ranges kernels.py:300-321)
+//   K1+update       (kernels.py:185-191, 398-399)
 //   K4 push scatter (kernels.py:285-297)
-//   K5 SpMV (kernels.py:412-487) reusing K2/K3/K4 with weights.
+//   K5 SpMV         (kernels.py:412-487), K2/K4 with weights.
+//
+// Iteration structure (pull): the blocks are gathered one launch at a time in
+// block order; each finished row is added straight into a dense f64 sums
+// vector at id_map[row] (sums[v] = ((0 + p_b0) + p_b1) + ... -- the
+// reference's block-ordered merge, kernels.py:310-320, without materialising
+// the partials arena), then one elementwise kernel applies the rank update,
+// the L1 delta, the next contributions and clears sums.  No two rows of a
+// block share a destination, and blocks are stream-ordered, so the
+// read-modify-write needs no atomics.
 //
 // Two arithmetic modes:
 //   exact (GCB_FLAG_EXACT): one thread per local row adds in storage order with
-//     __dadd_rn/__dmul_rn, the merge adds blocks in order from 0.0, the update
-//     is base + (d * s) with two roundings -> bit-identical to the reference.
+//     __dadd_rn/__dmul_rn, blocks merge in order from 0.0, the update is
+//     base + (d * s) with two roundings -> bit-identical to the reference.
 //   fast (default): edge-balanced warp tiles (merge-path): each lane owns
 //     kTileV consecutive edges, streams col_idx with 16-byte evict-first loads,
 //     gathers the L2-resident vertex values with evict-last loads, reduces
@@ -16,65 +25,35 @@
 //     irrelevant to load balance.  Results differ from the sequential order by
 //     reassociation only (|err| ~ 1e-15 relative).
 #include <cmath>
+#include <cstdlib>
 
 #include "gcb_internal.cuh"
 
 namespace gcb {
 
-// ---------------------------------------------------------------------------
-// cache-policy loads (sm_80+ createpolicy; evict_first for streams that are
-// read once, evict_last for the per-block vertex-value slice)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint4 ld_stream_u4(const void *ptr, uint64_t pol) {
-  uint4 r;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-      : "l"(ptr), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ double2 ld_stream_d2(const void *ptr, uint64_t pol) {
-  double2 r;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-      : "=d"(r.x), "=d"(r.y)
-      : "l"(ptr), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
-  double r;
-  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ double ld_keep(const float *p, uint64_t pol) {
-  float r;
-  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
-  return (double)r;
-}
+}  // namespace gcb
+
+#include "ldst.cuh"
+
+namespace gcb {
 
 constexpr int kWarps = 8;  // warps per CTA in the tile kernels
 
 // ---------------------------------------------------------------------------
 // K2 fast: edge-balanced pull gather over one block.
-//   partial_b[r] = sum_{e in row r} w_e * vals[col_e]  (w_e = 1 if unweighted)
-// Rows crossing a tile boundary: the tile where the row starts writes its
-// portion to partial_b[r]; every later tile writes its portion to carry_b[t];
-// k_fixup adds the carries in tile order.
+//   row_sum(r) = sum_{e in row r} w_e * vals[col_e]  (w_e = 1 if unweighted)
+//   ACCUM: out[id_map_b[r]] += row_sum(r)   (dense sums / y vector)
+//   else : out[r] = row_sum(r)              (partials of this block)
+// Rows crossing a tile boundary: the tile where the row starts emits its
+// portion as above; every later tile writes its portion to carry_b[t]; the
+// warp-per-span fix-up adds the carries afterwards.
 // ---------------------------------------------------------------------------
-template <typename VT, bool WGT>
+template <typename VT, bool WGT, bool ACCUM>
 __global__ void __launch_bounds__(kWarps * 32)
     k_pull_tiles(const uint32_t *__restrict__ col, const double *__restrict__ w,
-                 const uint32_t *__restrict__ lro_b, const uint32_t *__restrict__ tile_row,
-                 int64_t es, int64_t ee, int64_t t0, int64_t ntiles, uint32_t Lb,
-                 const VT *__restrict__ vals, double *__restrict__ partial_b,
+                 const uint32_t *__restrict__ lro_b, const uint32_t *__restrict__ id_map_b,
+                 const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
+                 int64_t ntiles, uint32_t Lb, const VT *__restrict__ vals, double *__restrict__ out,
                  double *__restrict__ carry_b) {
   constexpr int V = kTileV, T = kTileT;
   __shared__ uint32_t s_ends[kWarps][T + 32];
@@ -90,9 +69,9 @@ __global__ void __launch_bounds__(kWarps * 32)
     const int64_t llo = lbase > 0 ? lbase : 0;
     const int64_t lhi = (lbase + T < ee - es) ? lbase + T : ee - es;
     const uint32_t r0 = tile_row[t];
-    const uint32_t r0_start = lro_b[r0];
+    const bool r0_carried = (int64_t)lro_b[r0] < llo;
 
-    // issue the streaming loads first (independent of the row table)
+    // streaming loads first (independent of the row table)
     uint32_t c[V];
     {
       const uint4 *cp = reinterpret_cast<const uint4 *>(col + abase + lane * V);
@@ -129,6 +108,17 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
     __syncwarp();
 
+    auto emit = [&](int jj, double x) {
+      if (jj == 0 && r0_carried) {
+        carry_b[t] = x;
+      } else if (ACCUM) {
+        double *p = out + id_map_b[r0 + jj];
+        *p = __dadd_rn(*p, x);
+      } else {
+        out[r0 + jj] = x;
+      }
+    };
+
     const int64_t qf = q0 > llo ? q0 : llo;
     const bool lane_valid = (qf < lhi) && (q0 + V > llo);
     int j = 0;
@@ -154,7 +144,7 @@ __global__ void __launch_bounds__(kWarps * 32)
           head_sum = acc;
           head_closed = true;
         } else {
-          partial_b[r0 + j] = acc;  // middle row: starts and ends in this lane
+          emit(j, acc);  // middle row: starts and ends in this lane
         }
         acc = 0.0;
         ++j;
@@ -178,45 +168,43 @@ __global__ void __launch_bounds__(kWarps * 32)
     int nh = __shfl_down_sync(FULL, lane_valid ? head_j : -1000, 1);
     if (lane == 31) nh = -1000;
     if (lane_valid) {
-      if (head_closed) {
-        const double tot = (pk == head_j) ? __dadd_rn(pv, head_sum) : head_sum;
-        if (head_j == 0 && (int64_t)r0_start < llo) carry_b[t] = tot;
-        else partial_b[r0 + head_j] = tot;
-      }
-      if (nh != j) {
-        if (j == 0 && (int64_t)r0_start < llo) carry_b[t] = val;
-        else partial_b[r0 + j] = val;
-      }
+      if (head_closed) emit(head_j, (pk == head_j) ? __dadd_rn(pv, head_sum) : head_sum);
+      if (nh != j) emit(j, val);
     }
     __syncwarp();
   }
 }
 
-__global__ void k_fixup(int64_t nspans, const uint32_t *__restrict__ span_tile, int64_t tile_base,
-                        int64_t ntiles, const uint32_t *__restrict__ tile_row,
-                        const uint32_t *__restrict__ lro_b, int64_t t0, int64_t es,
-                        const double *__restrict__ carry_b, double *__restrict__ partial_b) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nspans;
-       s += (int64_t)gridDim.x * blockDim.x) {
+// Carry fix-up: one warp per row spanning several tiles; lanes sum the
+// carries in a fixed strided order, a fixed shuffle tree combines them.
+template <bool ACCUM>
+__global__ void k_fixup(int64_t nspans, const uint32_t *__restrict__ span_tile,
+                        const uint32_t *__restrict__ span_len, int64_t tile_base,
+                        const uint32_t *__restrict__ tile_row, const uint32_t *__restrict__ id_map_b,
+                        const double *__restrict__ carry_b, double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < nspans; s += nw) {
     const int64_t t = (int64_t)span_tile[s] - tile_base;
-    const uint32_t r = tile_row[t];
-    const uint32_t rstart = lro_b[r];
-    double acc = partial_b[r];
-    for (int64_t tt = t; tt < ntiles; ++tt) {
-      if (tile_row[tt] != r) break;
-      const int64_t q = (t0 + tt) * kTileT - es;
-      if ((int64_t)rstart >= q) break;
-      acc = __dadd_rn(acc, carry_b[tt]);
+    const uint32_t len = span_len[s];
+    double acc = 0.0;
+    for (uint32_t i = lane; i < len; i += 32) acc = __dadd_rn(acc, carry_b[t + i]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, d));
+    if (lane == 0) {
+      const uint32_t r = tile_row[t];
+      double *p = ACCUM ? out + id_map_b[r] : out + r;
+      *p = __dadd_rn(*p, acc);
     }
-    partial_b[r] = acc;
   }
 }
 
 // K2 exact: one thread per local row, storage order (kernels.py:155-170).
-template <bool WGT>
+template <bool WGT, bool ACCUM>
 __global__ void k_pull_exact(const uint32_t *__restrict__ col_b, const double *__restrict__ w_b,
-                             const uint32_t *__restrict__ lro_b, int64_t Lb,
-                             const double *__restrict__ vals, double *__restrict__ partial_b) {
+                             const uint32_t *__restrict__ lro_b, const uint32_t *__restrict__ id_map_b,
+                             int64_t Lb, const double *__restrict__ vals, double *__restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Lb;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -226,27 +214,25 @@ __global__ void k_pull_exact(const uint32_t *__restrict__ col_b, const double *_
       if (WGT) x = __dmul_rn(w_b[e], x);
       s = __dadd_rn(s, x);
     }
-    partial_b[i] = s;
+    if (ACCUM) {
+      double *p = out + id_map_b[i];
+      *p = __dadd_rn(*p, s);
+    } else {
+      out[i] = s;
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
-// K3: range-tiled merge (PAPER Fig. 5; accumulate_ranges kernels.py:300-321).
-// One CTA per kMergeK-wide destination range; block-ordered shared-memory
-// accumulation from 0.0, then the fused epilogue.
-//   MODE 0 (PageRank): r' = base + d*s; delta partial; c' = r'/deg (next
-//                      iteration's contributions, kernels.py:185-191)
-//   MODE 1 (SpMV / accumulate): y = s
+// K3: range-tiled merge of an explicit partials arena (accumulate_ranges,
+// kernels.py:300-321; PAPER Fig. 5).  One CTA per kMergeK-wide destination
+// range; block-ordered shared-memory accumulation from 0.0.
 // ---------------------------------------------------------------------------
-template <int MODE>
 __global__ void __launch_bounds__(512)
     k_merge(int64_t n, int64_t B, int64_t R, const int64_t *__restrict__ bounds,
             const uint32_t *__restrict__ id_map, const double *__restrict__ partial,
-            double *__restrict__ out, const uint32_t *__restrict__ deg, double base, double damping,
-            double *__restrict__ contrib, float *__restrict__ contrib32,
-            double *__restrict__ deltas) {
+            double *__restrict__ out) {
   __shared__ double buf[kMergeK];
-  __shared__ double red[32];
   const int64_t j = blockIdx.x;
   const int64_t lo = j * kMergeK;
   const int64_t hi = (lo + kMergeK < n) ? lo + kMergeK : n;
@@ -261,33 +247,7 @@ __global__ void __launch_bounds__(512)
     }
     __syncthreads();
   }
-  if (MODE == 1) {
-    for (int i = threadIdx.x; i < width; i += blockDim.x) out[lo + i] = buf[i];
-    return;
-  }
-  double dsum = 0.0;
-  for (int i = threadIdx.x; i < width; i += blockDim.x) {
-    const int64_t v = lo + i;
-    const double nr = __dadd_rn(base, __dmul_rn(damping, buf[i]));
-    const double old = out[v];
-    dsum += fabs(nr - old);
-    out[v] = nr;
-    const uint32_t dg = deg[v];
-    const double c = dg ? __ddiv_rn(nr, (double)dg) : 0.0;
-    if (contrib) contrib[v] = c;
-    if (contrib32) contrib32[v] = __double2float_rn(c);
-  }
-  // block reduction of the L1 delta
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, d);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dsum;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double x = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(0xffffffffu, x, d);
-    if (threadIdx.x == 0) deltas[j] = x;
-  }
+  for (int i = threadIdx.x; i < width; i += blockDim.x) out[lo + i] = buf[i];
 }
 
 // deterministic single-CTA sum of per-CTA partials
@@ -326,24 +286,64 @@ __global__ void k_pr_init(int64_t n, double r0, const uint32_t *__restrict__ deg
     const double c = dg ? __ddiv_rn(r0, (double)dg) : 0.0;
     if (contrib) contrib[v] = c;
     if (contrib32) contrib32[v] = __double2float_rn(c);
-    if (sums) sums[v] = 0.0;
+    sums[v] = 0.0;
   }
 }
 
-// push-direction rank update (kernels.py:398-399), resets sums for the next pass
-__global__ void k_pr_update_push(int64_t n, double base, double damping, double *__restrict__ sums,
-                                 double *__restrict__ ranks, const uint32_t *__restrict__ deg,
-                                 double *__restrict__ contrib, double *__restrict__ deltas) {
+// rank update (kernels.py:398-399) fused with the L1 delta (399), the next
+// iteration's contributions (185-191) and clearing sums for the next pass.
+__device__ __forceinline__ double pr_update_one(double s, double old, uint32_t dg, double base,
+                                                double damping, double &c, double &dsum) {
+  const double nr = __dadd_rn(base, __dmul_rn(damping, s));
+  dsum += fabs(nr - old);
+  c = dg ? __ddiv_rn(nr, (double)dg) : 0.0;
+  return nr;
+}
+
+__global__ void __launch_bounds__(256)
+    k_pr_update(int64_t n, double base, double damping, double *__restrict__ sums,
+                double *__restrict__ ranks, const uint32_t *__restrict__ deg,
+                double *__restrict__ contrib, float *__restrict__ contrib32,
+                double *__restrict__ deltas) {
   __shared__ double red[32];
   double dsum = 0.0;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+  // 4 vertices per thread per step with 16-byte vector accesses (n4 quads),
+  // scalar tail; all arrays come from cudaMalloc (256-byte aligned)
+  const int64_t n4 = n >> 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i << 2;
+    const double2 s01 = reinterpret_cast<const double2 *>(sums)[2 * i];
+    const double2 s23 = reinterpret_cast<const double2 *>(sums)[2 * i + 1];
+    const double2 o01 = reinterpret_cast<const double2 *>(ranks)[2 * i];
+    const double2 o23 = reinterpret_cast<const double2 *>(ranks)[2 * i + 1];
+    const uint4 d = reinterpret_cast<const uint4 *>(deg)[i];
+    double c0, c1, c2, c3;
+    const double2 n01 = make_double2(pr_update_one(s01.x, o01.x, d.x, base, damping, c0, dsum),
+                                     pr_update_one(s01.y, o01.y, d.y, base, damping, c1, dsum));
+    const double2 n23 = make_double2(pr_update_one(s23.x, o23.x, d.z, base, damping, c2, dsum),
+                                     pr_update_one(s23.y, o23.y, d.w, base, damping, c3, dsum));
+    reinterpret_cast<double2 *>(ranks)[2 * i] = n01;
+    reinterpret_cast<double2 *>(ranks)[2 * i + 1] = n23;
+    reinterpret_cast<double2 *>(sums)[2 * i] = make_double2(0.0, 0.0);
+    reinterpret_cast<double2 *>(sums)[2 * i + 1] = make_double2(0.0, 0.0);
+    if (contrib) {
+      reinterpret_cast<double2 *>(contrib)[2 * i] = make_double2(c0, c1);
+      reinterpret_cast<double2 *>(contrib)[2 * i + 1] = make_double2(c2, c3);
+    }
+    if (contrib32)
+      reinterpret_cast<float4 *>(contrib32)[i] =
+          make_float4(__double2float_rn(c0), __double2float_rn(c1), __double2float_rn(c2),
+                      __double2float_rn(c3));
+    (void)v;
+  }
+  for (int64_t v = (n4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const double nr = __dadd_rn(base, __dmul_rn(damping, sums[v]));
-    dsum += fabs(nr - ranks[v]);
-    ranks[v] = nr;
+    double c;
+    ranks[v] = pr_update_one(sums[v], ranks[v], deg[v], base, damping, c, dsum);
     sums[v] = 0.0;
-    const uint32_t dg = deg[v];
-    contrib[v] = dg ? __ddiv_rn(nr, (double)dg) : 0.0;
+    if (contrib) contrib[v] = c;
+    if (contrib32) contrib32[v] = __double2float_rn(c);
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, d);
@@ -493,69 +493,81 @@ static unsigned tile_grid(gcb_ctx *ctx, int64_t ntiles) {
   return (unsigned)(g < 1 ? 1 : g);
 }
 
-// per-block pull partials into bg->partials (block_only >= 0 -> one block)
+template <typename VT, bool WGT, bool ACCUM>
+static void launch_pull_tiles(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const VT *vals, double *out,
+                              bool window) {
+  const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+  const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
+  const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
+  const int64_t vlo = b * bg->width;
+  const int64_t vhi = (vlo + bg->width < bg->n) ? vlo + bg->width : bg->n;
+  launch_window(ctx, k_pull_tiles<VT, WGT, ACCUM>, tile_grid(ctx, nt), kWarps * 32, vals + vlo,
+                (size_t)(vhi - vlo) * sizeof(VT), window, (const uint32_t *)bg->col.p,
+                (const double *)(WGT ? bg->w.p : nullptr), (const uint32_t *)(bg->lro.p + rs + b),
+                (const uint32_t *)(bg->id_map.p + rs), (const uint32_t *)(bg->tile_row.p + tb), es,
+                ee, bg->h_tile_t0[b], nt, (uint32_t)Lb, vals, ACCUM ? out : out + rs,
+                bg->carry.p + tb);
+}
+
+// Pull gather of every block (or block_only) in block order.
+//   accum: out is a dense n-vector, out[id_map[row]] += row_sum (sums / y)
+//   else : out is the partials arena, out[arena_row] = row_sum
 void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *vals32,
-               bool use_weights, uint32_t flags, int64_t block_only) {
+               bool use_weights, uint32_t flags, int64_t block_only, double *out, bool accum) {
   ensure_derived(ctx, bg);
-  bg->partials.ensure(bg->L > 0 ? bg->L : 1);
   const bool exact = flags & GCB_FLAG_EXACT;
+  if (accum && !exact && vals && !vals32 && block_only < 0 && getenv("GCB_OLD_GATHER") == nullptr) {
+    gather_accum(ctx, bg, vals, use_weights, flags, out);  // gather.cu: hot-staged path
+    return;
+  }
   const bool window = !(flags & GCB_FLAG_NO_L2_WINDOW);
   const bool wgt = use_weights && bg->weighted;
   for (int64_t b = 0; b < bg->B; ++b) {
     if (block_only >= 0 && b != block_only) continue;
     const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
     if (Lb == 0) continue;
-    const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
+    const int64_t es = bg->h_edge_starts[b];
     const uint32_t *lro_b = bg->lro.p + rs + b;
-    double *part_b = bg->partials.p + rs;
-    if (exact || (vals32 == nullptr && vals == nullptr)) {
-      unsigned g = grid_for(Lb, 256, (int64_t)ctx->num_sms * 16);
-      if (wgt)
-        k_pull_exact<true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, bg->w.p + es, lro_b, Lb, vals,
-                                                        part_b);
+    const uint32_t *idm_b = bg->id_map.p + rs;
+    ProfScope ps_gather(ctx, 0);
+    if (exact || !(vals || vals32)) {
+      const unsigned g = grid_for(Lb, 256, (int64_t)ctx->num_sms * 16);
+      const double *wb = wgt ? bg->w.p + es : nullptr;
+      double *o = accum ? out : out + rs;
+      if (wgt && accum)
+        k_pull_exact<true, true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o);
+      else if (wgt)
+        k_pull_exact<true, false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o);
+      else if (accum)
+        k_pull_exact<false, true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o);
       else
-        k_pull_exact<false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, nullptr, lro_b, Lb, vals,
-                                                         part_b);
+        k_pull_exact<false, false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o);
       after_launch(ctx, "k_pull_exact");
       continue;
     }
-    const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
-    const int64_t t0 = bg->h_tile_t0[b];
-    const int64_t vlo = b * bg->width;
-    const int64_t vhi = (vlo + bg->width < bg->n) ? vlo + bg->width : bg->n;
-    const unsigned g = tile_grid(ctx, nt);
-    const uint32_t *trow = bg->tile_row.p + tb;
-    double *carry_b = bg->carry.p + tb;
-    const double *wp = wgt ? bg->w.p : nullptr;
-    ProfScope ps_gather(ctx, 0);
     if (vals32) {
-      const void *win = vals32 + vlo;
-      size_t wb = (size_t)(vhi - vlo) * sizeof(float);
-      if (wgt)
-        launch_window(ctx, k_pull_tiles<float, true>, g, kWarps * 32, win, wb, window,
-                      (const uint32_t *)bg->col.p, wp, lro_b, trow, es, ee, t0, nt, (uint32_t)Lb,
-                      vals32, part_b, carry_b);
-      else
-        launch_window(ctx, k_pull_tiles<float, false>, g, kWarps * 32, win, wb, window,
-                      (const uint32_t *)bg->col.p, wp, lro_b, trow, es, ee, t0, nt, (uint32_t)Lb,
-                      vals32, part_b, carry_b);
+      if (wgt && accum) launch_pull_tiles<float, true, true>(ctx, bg, b, vals32, out, window);
+      else if (wgt) launch_pull_tiles<float, true, false>(ctx, bg, b, vals32, out, window);
+      else if (accum) launch_pull_tiles<float, false, true>(ctx, bg, b, vals32, out, window);
+      else launch_pull_tiles<float, false, false>(ctx, bg, b, vals32, out, window);
     } else {
-      const void *win = vals + vlo;
-      size_t wb = (size_t)(vhi - vlo) * sizeof(double);
-      if (wgt)
-        launch_window(ctx, k_pull_tiles<double, true>, g, kWarps * 32, win, wb, window,
-                      (const uint32_t *)bg->col.p, wp, lro_b, trow, es, ee, t0, nt, (uint32_t)Lb,
-                      vals, part_b, carry_b);
-      else
-        launch_window(ctx, k_pull_tiles<double, false>, g, kWarps * 32, win, wb, window,
-                      (const uint32_t *)bg->col.p, wp, lro_b, trow, es, ee, t0, nt, (uint32_t)Lb,
-                      vals, part_b, carry_b);
+      if (wgt && accum) launch_pull_tiles<double, true, true>(ctx, bg, b, vals, out, window);
+      else if (wgt) launch_pull_tiles<double, true, false>(ctx, bg, b, vals, out, window);
+      else if (accum) launch_pull_tiles<double, false, true>(ctx, bg, b, vals, out, window);
+      else launch_pull_tiles<double, false, false>(ctx, bg, b, vals, out, window);
     }
     const int64_t sb = bg->h_span_base[b], ns = bg->h_span_base[b + 1] - sb;
     if (ns > 0) {
       ProfScope ps_fix(ctx, 1);
-      k_fixup<<<grid_for(ns, 128, 4096), 128, 0, ctx->stream>>>(
-          ns, bg->span_tile.p + sb, tb, nt, trow, lro_b, t0, es, carry_b, part_b);
+      const int64_t tb = bg->h_tile_base[b];
+      const unsigned g = grid_for(ns * 32, 256, (int64_t)ctx->num_sms * 8);
+      if (accum)
+        k_fixup<true><<<g, 256, 0, ctx->stream>>>(ns, bg->span_tile.p + sb, bg->span_len.p + sb, tb,
+                                                  bg->tile_row.p + tb, idm_b, bg->carry.p + tb, out);
+      else
+        k_fixup<false><<<g, 256, 0, ctx->stream>>>(ns, bg->span_tile.p + sb, bg->span_len.p + sb, tb,
+                                                   bg->tile_row.p + tb, idm_b, bg->carry.p + tb,
+                                                   out + rs);
       after_launch(ctx, "k_fixup");
     }
   }
@@ -564,10 +576,9 @@ void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *v
 void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out) {
   ensure_derived(ctx, bg);
   if (bg->R == 0) return;
-  k_merge<1><<<(unsigned)bg->R, 512, 0, ctx->stream>>>(bg->n, bg->B, bg->R, bg->bounds.p,
-                                                       bg->id_map.p, bg->partials.p, out, nullptr,
-                                                       0.0, 0.0, nullptr, nullptr, nullptr);
-  after_launch(ctx, "k_merge<1>");
+  k_merge<<<(unsigned)bg->R, 512, 0, ctx->stream>>>(bg->n, bg->B, bg->R, bg->bounds.p, bg->id_map.p,
+                                                    bg->partials.p, out);
+  after_launch(ctx, "k_merge");
 }
 
 void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sums, bool use_weights,
@@ -619,50 +630,46 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   ensure_derived(ctx, bg);
   const int64_t n = bg->n;
   const bool exact = flags & GCB_FLAG_EXACT;
-  const bool f32 = (flags & GCB_FLAG_F32_VALUES) && !exact && bg->direction == 0;
+  const bool push = bg->direction == 1;
+  const bool f32 = (flags & GCB_FLAG_F32_VALUES) && !exact && !push;
   const uint32_t *deg = deg_override ? deg_override : bg->deg.p;
   bg->contrib.ensure(n);
   if (f32) bg->contrib32.ensure(n);
-  const bool push = bg->direction == 1;
-  if (push) bg->sums.ensure(n);
+  bg->sums.ensure(n);
   const unsigned upd_grid = grid_for(n, 256, (int64_t)ctx->num_sms * 8);
-  bg->deltas.ensure((bg->R > (int64_t)upd_grid ? bg->R : (int64_t)upd_grid) + 2);
+  const int64_t nslots = (int64_t)upd_grid > 3 * (int64_t)ctx->num_sms ? (int64_t)upd_grid
+                                                                         : 3 * (int64_t)ctx->num_sms;
+  bg->deltas.ensure(nslots + 2);
   double *delta_dev = bg->deltas.p + bg->deltas.n - 1;
   const double r0 = 1.0 / (double)n;
   const double base = (1.0 - damping) / (double)n;
-  k_pr_init<<<grid_for(n, 256, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-      n, r0, deg, ranks_dev, bg->contrib.p, f32 ? bg->contrib32.p : nullptr,
-      push ? bg->sums.p : nullptr);
-  after_launch(ctx, "k_pr_init");
+  double *contrib = f32 ? nullptr : bg->contrib.p;
+  float *contrib32 = f32 ? bg->contrib32.p : nullptr;
+  {
+    ProfScope ps(ctx, 3);
+    k_pr_init<<<upd_grid, 256, 0, ctx->stream>>>(n, r0, deg, ranks_dev, bg->contrib.p, contrib32,
+                                                 bg->sums.p);
+    after_launch(ctx, "k_pr_init");
+  }
   double *hdelta = (double *)ctx->pinned;
   int it = 0, cv = 0;
   for (int k = 0; k < max_iters; ++k) {
-    int64_t ndeltas;
     if (!push) {
-      pull_sums(ctx, bg, bg->contrib.p, f32 ? bg->contrib32.p : nullptr, false, flags, -1);
-      if (bg->R > 0) {
-        ProfScope ps(ctx, 2);
-        k_merge<0><<<(unsigned)bg->R, 512, 0, ctx->stream>>>(
-            n, bg->B, bg->R, bg->bounds.p, bg->id_map.p, bg->partials.p, ranks_dev, deg, base,
-            damping, f32 ? nullptr : bg->contrib.p, f32 ? bg->contrib32.p : nullptr,
-            bg->deltas.p);
-        after_launch(ctx, "k_merge<0>");
-      }
-      ndeltas = bg->R;
+      pull_sums(ctx, bg, contrib, contrib32, false, flags, -1, bg->sums.p, true);
     } else {
-      {
-        ProfScope ps(ctx, 0);
-        push_scatter(ctx, bg, bg->contrib.p, bg->sums.p, false, flags, -1);
-      }
+      ProfScope ps(ctx, 0);
+      push_scatter(ctx, bg, bg->contrib.p, bg->sums.p, false, flags, -1);
+    }
+    {
       ProfScope ps(ctx, 2);
-      k_pr_update_push<<<upd_grid, 256, 0, ctx->stream>>>(n, base, damping, bg->sums.p, ranks_dev,
-                                                         deg, bg->contrib.p, bg->deltas.p);
-      after_launch(ctx, "k_pr_update_push");
-      ndeltas = upd_grid;
+      k_pr_update<<<upd_grid, 256, 0, ctx->stream>>>(n, base, damping, bg->sums.p, ranks_dev, deg,
+                                                     contrib ? contrib : (push ? bg->contrib.p : nullptr),
+                                                     contrib32, bg->deltas.p);
+      after_launch(ctx, "k_pr_update");
     }
     ++it;
     if (tol > 0.0) {
-      k_reduce_sum<<<1, 1024, 0, ctx->stream>>>(bg->deltas.p, ndeltas, delta_dev);
+      k_reduce_sum<<<1, 1024, 0, ctx->stream>>>(bg->deltas.p, upd_grid, delta_dev);
       after_launch(ctx, "k_reduce_sum");
       d2h(ctx, hdelta, delta_dev, 1);
       sync(ctx);
@@ -767,9 +774,11 @@ int gcb_process_block_pull(gcb_ctx *ctx, gcb_blocked *bg, int64_t block, const d
   DeviceGuard dg(ctx->device);
   ensure_derived(ctx, bg);
   bg->contrib.ensure(bg->n ? bg->n : 1);
+  bg->partials.ensure(bg->L > 0 ? bg->L : 1);
   h2d(ctx, bg->contrib.p, contrib_host, bg->n);
-  pull_sums(ctx, bg, bg->contrib.p, nullptr, false, flags, block);
   const int64_t rs = bg->h_row_starts[block], Lb = bg->h_row_starts[block + 1] - rs;
+  GCB_CUDA(cudaMemsetAsync(bg->partials.p + rs, 0, (Lb ? Lb : 1) * sizeof(double), ctx->stream));
+  pull_sums(ctx, bg, bg->contrib.p, nullptr, false, flags, block, bg->partials.p, false);
   d2h(ctx, out_host, bg->partials.p + rs, Lb);
   sync(ctx);
   GCB_API_END
@@ -784,12 +793,12 @@ int gcb_process_block_push(gcb_ctx *ctx, gcb_blocked *bg, int64_t block, const d
   ensure_derived(ctx, bg);
   const int64_t n = bg->n;
   bg->contrib.ensure(n ? n : 1);
-  bg->sums.ensure(n ? n : 1);
   DArray<double> local(n ? n : 1), dsums(n ? n : 1);
   h2d(ctx, bg->contrib.p, contrib_host, n);
   h2d(ctx, dsums.p, sums_host, n);
   GCB_CUDA(cudaMemsetAsync(local.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));
-  push_scatter(ctx, bg, bg->contrib.p, local.p, false, flags, block);  // unweighted (kernels.py:291-293)
+  // unweighted, like the reference (kernels.py:291-293)
+  push_scatter(ctx, bg, bg->contrib.p, local.p, false, flags, block);
   const int64_t lo = block * bg->width, hi = (lo + bg->width < n) ? lo + bg->width : n;
   if (hi > lo) {
     k_add_range<<<grid_for(hi - lo, 256, 4096), 256, 0, ctx->stream>>>(lo, hi, local.p, dsums.p);
@@ -816,6 +825,13 @@ int gcb_accumulate_ranges(gcb_ctx *ctx, gcb_blocked *bg, const double *partials_
   GCB_API_END
 }
 
+// y = pull gather of x over a blocking, accumulated block by block
+static void pull_spmv(gcb_ctx *ctx, gcb_blocked *bg, const double *x, bool weights, uint32_t flags,
+                      double *y) {
+  GCB_CUDA(cudaMemsetAsync(y, 0, (bg->n ? bg->n : 1) * sizeof(double), ctx->stream));
+  pull_sums(ctx, bg, x, nullptr, weights, flags, -1, y, true);
+}
+
 int gcb_segment_row_sums(gcb_ctx *ctx, const gcb_csr *g, const double *values_host, int use_weights,
                          uint32_t flags, double *out_host) {
   GCB_API_BEGIN
@@ -824,8 +840,7 @@ int gcb_segment_row_sums(gcb_ctx *ctx, const gcb_csr *g, const double *values_ho
   gcb_blocked *v = compact_for(ctx, g, 0);
   DArray<double> x(g->n ? g->n : 1), y(g->n ? g->n : 1);
   h2d(ctx, x.p, values_host, g->n);
-  pull_sums(ctx, v, x.p, nullptr, use_weights != 0, flags, -1);
-  merge_to(ctx, v, y.p);
+  pull_spmv(ctx, v, x.p, use_weights != 0, flags, y.p);
   d2h(ctx, out_host, y.p, g->n);
   sync(ctx);
   GCB_API_END
@@ -841,8 +856,7 @@ int gcb_spmv(gcb_ctx *ctx, const gcb_csr *g, const double *x_host, int direction
   DArray<double> x(g->n ? g->n : 1), y(g->n ? g->n : 1);
   h2d(ctx, x.p, x_host, g->n);
   if (direction == 0) {
-    pull_sums(ctx, v, x.p, nullptr, true, flags, -1);
-    merge_to(ctx, v, y.p);
+    pull_spmv(ctx, v, x.p, true, flags, y.p);
   } else {
     GCB_CUDA(cudaMemsetAsync(y.p, 0, (g->n ? g->n : 1) * sizeof(double), ctx->stream));
     push_scatter(ctx, v, x.p, y.p, true, flags, -1);
@@ -856,9 +870,7 @@ static void spmv_blocked_dev(gcb_ctx *ctx, gcb_blocked *bg, const double *x, uin
                              double *y) {
   ensure_derived(ctx, bg);
   if (bg->direction == 0) {
-    pull_sums(ctx, bg, x, nullptr, true, flags, -1);
-    if (bg->R == 0) return;
-    merge_to(ctx, bg, y);
+    pull_spmv(ctx, bg, x, true, flags, y);
   } else {
     GCB_CUDA(cudaMemsetAsync(y, 0, (bg->n ? bg->n : 1) * sizeof(double), ctx->stream));
     push_scatter(ctx, bg, x, y, true, flags, -1);
