@@ -636,7 +636,9 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   bg->contrib.ensure(n);
   if (f32) bg->contrib32.ensure(n);
   bg->sums.ensure(n);
-  const unsigned upd_grid = grid_for(n, 256, (int64_t)ctx->num_sms * 8);
+  // one 4-vertex quad per thread: enough loads in flight to run at HBM speed
+  // (a capped grid-stride loop left this pass latency-bound, 0.26 IPC in ncu)
+  const unsigned upd_grid = grid_for((n + 3) / 4, 256, 1 << 20);
   const int64_t nslots = (int64_t)upd_grid > 3 * (int64_t)ctx->num_sms ? (int64_t)upd_grid
                                                                          : 3 * (int64_t)ctx->num_sms;
   bg->deltas.ensure(nslots + 2);
