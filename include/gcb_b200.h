@@ -187,6 +187,14 @@ int gcb_bfs(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t source
             uint32_t *level_verts_host, int64_t *level_sizes_host,
             uint8_t *directions_host, int64_t max_levels, int64_t *num_levels,
             int64_t *num_expansions);
+/* One level of the forward sweep: direction 0 = forward_push_step
+ * traversal.py:121-140 over g, 1 = forward_pull_step traversal.py:143-176
+ * over bg_pull.  depth[n] (in/out), sigma[n] (in/out, NULL = no path counts),
+ * frontier = current queue; writes the next queue (ascending) to next_host
+ * and its length to *next_size; discovered vertices get depth level + 1. */
+int gcb_bfs_step(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int direction,
+                 int32_t *depth_host, double *sigma_host_or_null, const uint32_t *frontier_host,
+                 int64_t frontier_size, int32_t level, uint32_t *next_host, int64_t *next_size);
 /* SSSP with non-negative integer weights (named by BASELINE.json; no
  * reference code).  The weights are the graphs' edge weights
  * (integral float64 < 2^53): g = weighted forward CSR, bg_pull =

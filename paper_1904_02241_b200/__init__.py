@@ -58,6 +58,8 @@ from .traversal import (
     TraversalState,
     bfs,
     choose_direction,
+    forward_pull_step,
+    forward_push_step,
     sample_sources,
     sssp,
 )

@@ -81,6 +81,8 @@ SIGNATURES = {
     "gcb_spmv_blocked_dev": ([c_vp, c_vp, c_vp, c_u32, c_vp], c_int),
     "gcb_bfs": ([c_vp, c_vp, c_vp, c_i64, c_int, c_i64, c_i64, P_i32, P_u32, P_i64, P_u8, c_i64,
                  P_i64, P_i64], c_int),
+    "gcb_bfs_step": ([c_vp, c_vp, c_vp, c_int, P_i32, P_dbl, P_u32, c_i64, ctypes.c_int32, P_u32,
+                      P_i64], c_int),
     "gcb_sssp": ([c_vp, c_vp, c_vp, c_i64, c_int, c_i64, c_i64, P_i64, P_u8, c_i64, P_i64], c_int),
     "gcb_cc": ([c_vp, c_vp, P_u32, P_i64], c_int),
 }

@@ -533,3 +533,151 @@ int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_c
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Single level steps with path counts (forward_push_step traversal.py:121-140,
+// forward_pull_step traversal.py:143-176).  sigma values are integer-valued
+// doubles (< 2^53), so the atomic sums are exact in any order.
+// ---------------------------------------------------------------------------
+namespace gcb {
+
+__global__ void k_step_push(int64_t qsize, const uint32_t *__restrict__ queue,
+                            const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
+                            const int32_t *__restrict__ depth, const double *__restrict__ sigma,
+                            uint8_t *__restrict__ next, double *__restrict__ sig_add) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < qsize; i += nw) {
+    const uint32_t u = queue[i];
+    const double su = sigma ? sigma[u] : 0.0;
+    for (int64_t k = ro[u] + lane; k < ro[u + 1]; k += 32) {
+      const uint32_t v = col[k];
+      if (depth[v] == kInfDepth) {
+        next[v] = 1;
+        if (sigma) atomicAdd(sig_add + v, su);
+      }
+    }
+  }
+}
+
+// per block: unvisited rows sum sigma (or 1) over in-range frontier sources
+__global__ void k_step_pull(int64_t Lb, const uint32_t *__restrict__ lro_b,
+                            const uint32_t *__restrict__ id_map_b, const uint32_t *__restrict__ col_b,
+                            const uint32_t *__restrict__ front_bits, const int32_t *__restrict__ depth,
+                            const double *__restrict__ sigma, uint8_t *__restrict__ next,
+                            double *__restrict__ sig_add) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Lb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = id_map_b[i];
+    if (depth[v] != kInfDepth) continue;
+    double s = 0.0;
+    for (uint32_t e = lro_b[i]; e < lro_b[i + 1]; ++e) {
+      const uint32_t u = col_b[e];
+      if (front_bits[u >> 5] >> (u & 31) & 1u) {
+        if (!sigma) {
+          s = 1.0;
+          break;
+        }
+        s += sigma[u];
+      }
+    }
+    if (s > 0.0) {
+      next[v] = 1;
+      if (sigma) atomicAdd(sig_add + v, s);
+    }
+  }
+}
+
+__global__ void k_step_commit(int64_t n, int32_t level, uint8_t *__restrict__ next,
+                              const uint32_t *__restrict__ pos, uint32_t *__restrict__ queue_out,
+                              int32_t *__restrict__ depth, double *__restrict__ sigma,
+                              double *__restrict__ sig_add) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (!next[v]) continue;
+    queue_out[pos[v]] = (uint32_t)v;
+    depth[v] = level;
+    next[v] = 0;
+    if (sigma) {
+      sigma[v] += sig_add[v];
+      sig_add[v] = 0.0;
+    }
+  }
+}
+
+__global__ void k_set_bits(int64_t q, const uint32_t *__restrict__ queue, uint32_t *__restrict__ bits) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicOr(bits + (queue[i] >> 5), 1u << (queue[i] & 31));
+}
+
+}  // namespace gcb
+
+extern "C" int gcb_bfs_step(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int direction,
+                            int32_t *depth_host, double *sigma_host_or_null,
+                            const uint32_t *frontier_host, int64_t frontier_size, int32_t level,
+                            uint32_t *next_host, int64_t *next_size) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && depth_host && next_size && (frontier_host || frontier_size == 0), "NULL argument");
+  GCB_REQUIRE(direction == 0 || direction == 1, "direction must be push (0) or pull (1)");
+  GCB_REQUIRE(direction == 0 ? g != nullptr : bg_pull != nullptr, "missing graph for the step");
+  DeviceGuard dg(ctx->device);
+  const int64_t n = direction == 0 ? g->n : bg_pull->n;
+  DArray<int32_t> depth(n ? n : 1);
+  DArray<double> sigma, sig_add;
+  DArray<uint32_t> queue(frontier_size ? frontier_size : 1), out(n ? n : 1);
+  Frontier F(n);
+  h2d(ctx, depth.p, depth_host, n);
+  h2d(ctx, queue.p, frontier_host, frontier_size);
+  GCB_CUDA(cudaMemsetAsync(F.next.p, 0, n ? n : 1, ctx->stream));
+  if (sigma_host_or_null) {
+    sigma.alloc(n ? n : 1);
+    sig_add.alloc(n ? n : 1);
+    h2d(ctx, sigma.p, sigma_host_or_null, n);
+    GCB_CUDA(cudaMemsetAsync(sig_add.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));
+  }
+  double *sg = sigma_host_or_null ? sigma.p : nullptr;
+  if (direction == 0) {
+    if (frontier_size) {
+      k_step_push<<<grid_for(frontier_size * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0,
+                    ctx->stream>>>(frontier_size, queue.p, g->ro.p, g->col.p, depth.p, sg, F.next.p,
+                                   sig_add.p);
+      after_launch(ctx, "k_step_push");
+    }
+  } else {
+    gcb_blocked *bg = bg_pull;
+    GCB_REQUIRE(bg->direction == 0, "g_blocked must be a pull blocking");
+    ensure_derived(ctx, bg);
+    GCB_CUDA(cudaMemsetAsync(F.bits.p, 0, ((n + 31) / 32 + 1) * sizeof(uint32_t), ctx->stream));
+    if (frontier_size) {
+      k_set_bits<<<grid_for(frontier_size, 256, 4096), 256, 0, ctx->stream>>>(frontier_size, queue.p,
+                                                                             F.bits.p);
+      after_launch(ctx, "k_set_bits");
+    }
+    for (int64_t b = 0; b < bg->B; ++b) {
+      const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+      if (!Lb) continue;
+      k_step_pull<<<grid_for(Lb, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          Lb, bg->lro.p + rs + b, bg->id_map.p + rs, bg->col.p + bg->h_edge_starts[b], F.bits.p,
+          depth.p, sg, F.next.p, sig_add.p);
+      after_launch(ctx, "k_step_pull");
+    }
+  }
+  k_flags_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, F.next.p, F.flags.p);
+  after_launch(ctx, "k_flags_u32");
+  GCB_CUDA(cudaMemsetAsync(F.flags.p + n, 0, sizeof(uint32_t), ctx->stream));
+  cub_exclusive_sum_u32(ctx, F.flags.p, F.pos.p, n + 1);
+  k_step_commit<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, level + 1, F.next.p, F.pos.p,
+                                                                  out.p, depth.p, sg, sig_add.p);
+  after_launch(ctx, "k_step_commit");
+  uint32_t cnt = 0;
+  d2h(ctx, &cnt, F.pos.p + n, 1);
+  sync(ctx);
+  *next_size = cnt;
+  d2h(ctx, depth_host, depth.p, n);
+  if (sigma_host_or_null) d2h(ctx, sigma_host_or_null, sigma.p, n);
+  if (next_host) d2h(ctx, next_host, out.p, cnt);
+  sync(ctx);
+  GCB_API_END
+}

@@ -26,6 +26,8 @@ __all__ = [
     "BfsResult",
     "SsspResult",
     "choose_direction",
+    "forward_push_step",
+    "forward_pull_step",
     "bfs",
     "sssp",
     "sample_sources",
@@ -96,6 +98,40 @@ def choose_direction(g: CsrGraph, state: TraversalState, policy: DirectionPolicy
         return "blocked-pull"
     working_set = int(g.out_degrees[state.frontier].sum()) * policy.value_bytes
     return "blocked-pull" if working_set > policy.cache_capacity_bytes else "push"
+
+
+def _step(direction: int, g, bg, state: TraversalState, accumulate_sigma: bool) -> np.ndarray:
+    handle = g.device() if direction == 0 else bg.device()
+    ctx = handle.ctx
+    depth = np.ascontiguousarray(state.depth, dtype=np.int32)
+    sigma = np.ascontiguousarray(state.sigma, dtype=np.float64) if accumulate_sigma else None
+    front = np.ascontiguousarray(state.frontier, dtype=np.uint32)
+    nxt = np.empty(depth.size, dtype=np.uint32)
+    cnt = ctypes.c_int64()
+    _lib.check(ctx._lib.gcb_bfs_step(
+        ctx.handle, g.device().raw if direction == 0 else None,
+        bg.device().raw if direction == 1 else None, direction, _lib.ptr(depth, _lib.P_i32),
+        _lib.ptr(sigma, _lib.P_dbl), _lib.ptr(front, _lib.P_u32), front.size, int(state.level),
+        _lib.ptr(nxt, _lib.P_u32), ctypes.byref(cnt)), "bfs step")
+    state.depth[...] = depth
+    if accumulate_sigma:
+        state.sigma[...] = sigma
+    q = nxt[: cnt.value].copy()
+    state.frontier = q
+    state.level += 1
+    return q
+
+
+def forward_push_step(g: CsrGraph, state: TraversalState, accumulate_sigma: bool):
+    """One top-down level over the frontier queue (traversal.py:121-140)."""
+    return _step(0, g, None, state, accumulate_sigma)
+
+
+def forward_pull_step(g_blocked: BlockedGraph, state: TraversalState, accumulate_sigma: bool):
+    """One bottom-up level over the TOCAB blocks of the transpose
+    (traversal.py:143-176): every unvisited row sums sigma (or 1) over its
+    in-range frontier sources; discovered rows join the next level."""
+    return _step(1, None, g_blocked, state, accumulate_sigma)
 
 
 def _check_source(g: CsrGraph, source: int):
