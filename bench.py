@@ -176,7 +176,7 @@ def run_reference(args):
     line = {
         "metric": "PageRank GTEPS per iteration", "value": round(value, 6), "unit": "GTEPS",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic R-MAT (reference generator)",
         "config": workload_config(args, n, m),
         "cpu_baseline": {"value": round(value, 6), "unit": "GTEPS", "cores": threads,
@@ -196,7 +196,8 @@ def workload_config(args, n, m):
         "iterations_per_step": args.iters, "damping": 0.85, "tol": 0.0,
         "direction": args.direction, "value_dtype": "f32" if args.f32_values else "f64",
         "l2": "inputs larger than L2 (col arena 4|E| bytes >> 126 MB)",
-        "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU",
+        "parallelism": (f"destination shards x{args.gpus} (equal in-edges), NCCL all-gather of "
+                        "contributions" if args.gpus > 1 else "single GPU"),
     }
 
 
@@ -213,10 +214,16 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GCB_DEVICE / GCB_DIST_BACKEND let the multi-rank path be smoke-tested
+    # with several ranks on one GPU (gloo); production is one rank per GPU, NCCL
+    local = int(os.environ.get("GCB_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("GCB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     ctx = _lib.context(local)
     # a real (non-legacy) stream shared by the library and the timing events
     stream = torch.cuda.Stream(device=local)
@@ -225,14 +232,6 @@ def run_ours(args):
 
     # ---- setup (untimed): device R-MAT -> transpose -> TOCAB partition ----
     t0 = time.perf_counter()
-    if args.direction == "pull":
-        src = gcb.generate_rmat(args.scale, args.edge_factor, args.seed, transposed=True)
-    else:
-        src = gcb.generate_rmat(args.scale, args.edge_factor, args.seed)
-    bg = gcb.partition_tocab(src, args.direction, args.width)
-    n, m = bg.num_vertices, bg.num_edges
-    del src
-    h = bg.device()
     flags = 0
     if args.exact:
         flags |= _lib.FLAG_EXACT
@@ -240,13 +239,39 @@ def run_ours(args):
         flags |= _lib.FLAG_F32_VALUES
     if args.no_l2_window:
         flags |= _lib.FLAG_NO_L2_WINDOW
-    ranks = torch.empty(n, dtype=torch.float64, device=f"cuda:{local}")
-    it, cv = ctypes.c_int(), ctypes.c_int()
+    if args.direction == "pull":
+        src = gcb.generate_rmat(args.scale, args.edge_factor, args.seed, transposed=True)
+    else:
+        src = gcb.generate_rmat(args.scale, args.edge_factor, args.seed)
+    if world > 1:
+        # strong scaling: every rank builds the same graph and owns an
+        # equal-in-edge destination range (parallel.py)
+        from paper_1904_02241_b200 import parallel
 
-    def step():
-        _lib.check(ctx._lib.gcb_pr_blocked_dev(ctx.handle, h.raw, 0.85, 0.0, args.iters, flags,
-                                               ctypes.c_void_p(ranks.data_ptr()),
-                                               ctypes.byref(it), ctypes.byref(cv)))
+        if args.direction != "pull":
+            raise SystemExit("multi-GPU PageRank shards the pull direction")
+        plan = parallel.ShardPlan(parallel.shard_ranges(src.row_offsets, world))
+        engine = parallel.DeviceShard(src, *plan.owned(rank), args.width, flags)
+        runner = parallel.ShardedPageRank(engine, plan, rank, parallel.TorchExchange(plan, rank))
+        n, m = src.num_vertices, src.num_edges
+        bg = engine.bg
+        del src
+        params = gcb.PrParams(tol=0.0, max_iters=args.iters)
+
+        def step():
+            runner.run(params, gather_ranks=False)
+    else:
+        bg = gcb.partition_tocab(src, args.direction, args.width)
+        n, m = bg.num_vertices, bg.num_edges
+        del src
+        h = bg.device()
+        ranks = torch.empty(n, dtype=torch.float64, device=f"cuda:{local}")
+        it, cv = ctypes.c_int(), ctypes.c_int()
+
+        def step():
+            _lib.check(ctx._lib.gcb_pr_blocked_dev(ctx.handle, h.raw, 0.85, 0.0, args.iters,
+                                                   flags, ctypes.c_void_p(ranks.data_ptr()),
+                                                   ctypes.byref(it), ctypes.byref(cv)))
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -278,8 +303,8 @@ def run_ours(args):
         dist.barrier()
     ms_step = ms_total / args.steps
     t_iter_s = ms_step / 1e3 / args.iters
-    gteps_rank = m / t_iter_s / 1e9
-    value = gteps_rank * world
+    # the whole graph (m edges) is processed once per iteration by the job
+    value = m / t_iter_s / 1e9
 
     # ---- per-kernel breakdown (separate, profiled pass; not the timed number) ----
     ctx.set_profiling(True)
@@ -293,6 +318,7 @@ def run_ours(args):
     gather_groups = prof["gather"][1] / (prof_steps * args.iters)
 
     peak, peak_kind = measured_hbm_peak()
+    peak *= world  # aggregate HBM of the job
     b_alg = algorithmic_bytes_pr(n, m)
     achieved = b_alg / t_iter_s / 1e9
     # gather kernel alone: its share of the algorithmic bytes = col + contributions read
@@ -321,7 +347,7 @@ def run_ours(args):
 
     # ---- e2e: public host-buffer API, arenas from pinned memory each step ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         e2e = run_e2e(args, bg, ctx, stream, flags)
 
     cpu = None
@@ -342,7 +368,7 @@ def run_ours(args):
             "metric": "PageRank GTEPS per iteration", "value": round(value, 3), "unit": "GTEPS",
             "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic R-MAT generated on device (bit-exact with the reference)",
             "config": workload_config(args, n, m),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -105,6 +105,12 @@ int gcb_csr_symmetrize(gcb_ctx *ctx, const gcb_csr *g, gcb_csr **out);
 int gcb_csr_info(const gcb_csr *g, int64_t *n, int64_t *m, int *weighted);
 int gcb_csr_download(gcb_ctx *ctx, const gcb_csr *g, int64_t *row_offsets_host,
                      uint32_t *col_host, double *weights_host_or_null);
+/* rows [v0, v1) of g, all other rows emptied (n x n): a destination shard's
+ * slab of the transpose */
+int gcb_csr_row_slab(gcb_ctx *ctx, const gcb_csr *g, int64_t v0, int64_t v1, gcb_csr **out);
+/* counts_dev[v] (device uint32[n]) = occurrences of v in the column ids;
+ * for the transpose these are the forward out-degrees (kernels.py:199-204) */
+int gcb_csr_col_counts(gcb_ctx *ctx, const gcb_csr *g, uint32_t *counts_dev);
 /* set/replace the edge weights of a device CSR (storage order) */
 int gcb_csr_set_weights(gcb_ctx *ctx, gcb_csr *g, const double *weights_host);
 int gcb_csr_destroy(gcb_csr *g);
@@ -152,6 +158,19 @@ int gcb_pr_baseline(gcb_ctx *ctx, const gcb_csr *g, int direction, double dampin
                     double tol, int max_iters, uint32_t flags,
                     const int64_t *out_degrees_host_or_null, double *ranks_host,
                     int *iterations, int *converged);
+/* Destination-sharded PageRank (multi-GPU).  Rank r owns
+ * [v0, v1) (v0 % 4 == 0) and a pull blocking of its row slab; contrib_dev and
+ * ranks_dev are full n-vectors on the device, deg_dev the global
+ * out-degrees.  init sets ranks/contributions of the owned slice; step
+ * gathers over the full contribution vector, then updates the owned slice of
+ * ranks and contributions in place and (if delta_dev) writes the slice's L1
+ * delta.  The caller all-gathers the owned contribution slices between steps
+ * (NCCL).  Both calls are stream-ordered and do not synchronise. */
+int gcb_pr_shard_init(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1,
+                      const uint32_t *deg_dev, double *contrib_dev, double *ranks_dev);
+int gcb_pr_shard_step(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, double damping,
+                      uint32_t flags, const uint32_t *deg_dev, double *contrib_dev,
+                      double *ranks_dev, double *delta_dev);
 /* process_block_pull kernels.py:275-282: partials of block b (n_local f64) */
 int gcb_process_block_pull(gcb_ctx *ctx, gcb_blocked *bg, int64_t block,
                            const double *contrib_host, uint32_t flags,

@@ -59,6 +59,10 @@ SIGNATURES = {
     "gcb_csr_info": ([c_vp, P_i64, P_i64, P_int], c_int),
     "gcb_csr_download": ([c_vp, c_vp, P_i64, P_u32, P_dbl], c_int),
     "gcb_csr_set_weights": ([c_vp, c_vp, P_dbl], c_int),
+    "gcb_csr_row_slab": ([c_vp, c_vp, c_i64, c_i64, PP], c_int),
+    "gcb_csr_col_counts": ([c_vp, c_vp, c_vp], c_int),
+    "gcb_pr_shard_init": ([c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp], c_int),
+    "gcb_pr_shard_step": ([c_vp, c_vp, c_i64, c_i64, c_dbl, c_u32, c_vp, c_vp, c_vp, c_vp], c_int),
     "gcb_csr_destroy": ([c_vp], c_int),
     "gcb_partition_tocab": ([c_vp, c_vp, c_int, c_i64, PP], c_int),
     "gcb_blocked_upload": ([c_vp, c_int, c_i64, c_i64, c_i64, c_i64, P_i64, P_i64, P_u32, P_i64,
@@ -171,6 +175,15 @@ class Context:
         check(self._lib.gcb_ctx_read_profile(self.handle, ms, cnt))
         names = ("gather", "fixup", "merge", "other")
         return {k: (ms[i], cnt[i]) for i, k in enumerate(names)}
+
+    def bind_torch_stream(self):
+        """Run on torch's current stream of this device so library kernels
+        order with torch copies / NCCL collectives (the legacy default stream
+        has handle 0, passed to CUDA as cudaStreamLegacy = 0x1)."""
+        import torch
+
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        self.set_stream(s if s else 1)
 
     def set_stream(self, stream_ptr: int | None):
         check(self._lib.gcb_ctx_set_stream(self.handle, c_vp(stream_ptr or 0)))

@@ -448,4 +448,75 @@ int gcb_csr_destroy(gcb_csr *g) {
   GCB_API_END
 }
 
+__global__ void k_slab_offsets(int64_t n, int64_t v0, int64_t v1, const int64_t *__restrict__ ro,
+                               int64_t *__restrict__ out) {
+  const int64_t lo = ro[v0], hi = ro[v1];
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x = ro[v];
+    x = x < lo ? lo : (x > hi ? hi : x);
+    out[v] = x - lo;
+  }
+}
+
+__global__ void k_col_counts(int64_t m, const uint32_t *__restrict__ col, uint32_t *__restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + col[i], 1u);
+}
+
+// rows [v0, v1) of g kept, every other row emptied (same n x n shape): the
+// slab a destination shard owns
+int gcb_csr_row_slab(gcb_ctx *ctx, const gcb_csr *g, int64_t v0, int64_t v1, gcb_csr **out) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && out, "NULL argument");
+  GCB_REQUIRE(0 <= v0 && v0 <= v1 && v1 <= g->n, "bad row range");
+  DeviceGuard dg(ctx->device);
+  int64_t se[2];
+  d2h(ctx, &se[0], g->ro.p + v0, 1);
+  d2h(ctx, &se[1], g->ro.p + v1, 1);
+  sync(ctx);
+  const int64_t m = se[1] - se[0];
+  auto s = new gcb_csr();
+  try {
+    s->device = ctx->device;
+    s->n = g->n;
+    s->m = m;
+    s->ro.alloc(g->n + 1);
+    s->col.alloc(m + kColPad);
+    GCB_CUDA(cudaMemsetAsync(s->col.p + m, 0, kColPad * sizeof(uint32_t), ctx->stream));
+    k_slab_offsets<<<grid_for(g->n + 1, 256, 65536), 256, 0, ctx->stream>>>(g->n, v0, v1, g->ro.p,
+                                                                           s->ro.p);
+    after_launch(ctx, "k_slab_offsets");
+    if (m) GCB_CUDA(cudaMemcpyAsync(s->col.p, g->col.p + se[0], m * sizeof(uint32_t),
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+    if (g->weighted) {
+      s->weighted = true;
+      s->w.alloc(m + kColPad);
+      if (m) GCB_CUDA(cudaMemcpyAsync(s->w.p, g->w.p + se[0], m * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    sync(ctx);
+  } catch (...) {
+    delete s;
+    throw;
+  }
+  *out = s;
+  GCB_API_END
+}
+
+// counts[v] = occurrences of v among the column ids (for the transpose: the
+// forward out-degrees, kernels.py:199-204); counts_dev is a device uint32[n]
+int gcb_csr_col_counts(gcb_ctx *ctx, const gcb_csr *g, uint32_t *counts_dev) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && counts_dev, "NULL argument");
+  DeviceGuard dg(ctx->device);
+  GCB_CUDA(cudaMemsetAsync(counts_dev, 0, (g->n ? g->n : 1) * sizeof(uint32_t), ctx->stream));
+  if (g->m) {
+    k_col_counts<<<grid_for(g->m, 256, 65536), 256, 0, ctx->stream>>>(g->m, g->col.p, counts_dev);
+    after_launch(ctx, "k_col_counts");
+  }
+  GCB_API_END
+}
+
 }  // extern "C"

@@ -902,4 +902,63 @@ int gcb_spmv_blocked_dev(gcb_ctx *ctx, gcb_blocked *bg, const double *x_dev, uin
   GCB_API_END
 }
 
+// ---------------------------------------------------------------------------
+// Destination-sharded PageRank: rank r owns vertices [v0, v1) of
+// the transpose; its blocking holds only those rows, the contribution vector
+// is the full n-vector kept in sync by the caller's all-gather of every
+// rank's [v0, v1) slice.  deg_dev = global out-degrees (gcb_csr_col_counts).
+// ---------------------------------------------------------------------------
+int gcb_pr_shard_init(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, const uint32_t *deg_dev,
+                      double *contrib_dev, double *ranks_dev) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && deg_dev && contrib_dev && ranks_dev, "NULL argument");
+  GCB_REQUIRE(0 <= v0 && v0 <= v1 && v1 <= bg->n && bg->n > 0, "bad shard range");
+  GCB_REQUIRE(bg->direction == 0, "sharded PageRank runs on a pull blocking");
+  DeviceGuard dg(ctx->device);
+  ensure_derived(ctx, bg);
+  bg->sums.ensure(bg->n);
+  GCB_CUDA(cudaMemsetAsync(bg->sums.p, 0, bg->n * sizeof(double), ctx->stream));
+  const int64_t cnt = v1 - v0;
+  if (cnt) {
+    k_pr_init<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(
+        cnt, 1.0 / (double)bg->n, deg_dev + v0, ranks_dev + v0, contrib_dev + v0, nullptr,
+        bg->sums.p + v0);
+    after_launch(ctx, "k_pr_init");
+  }
+  GCB_API_END
+}
+
+int gcb_pr_shard_step(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, double damping,
+                      uint32_t flags, const uint32_t *deg_dev, double *contrib_dev,
+                      double *ranks_dev, double *delta_dev) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && deg_dev && contrib_dev && ranks_dev, "NULL argument");
+  GCB_REQUIRE(0 <= v0 && v0 <= v1 && v1 <= bg->n && (v0 % 4) == 0, "bad shard range");
+  DeviceGuard dg(ctx->device);
+  ensure_derived(ctx, bg);
+  bg->sums.ensure(bg->n);
+  const int64_t cnt = v1 - v0;
+  const unsigned grid = grid_for((cnt + 3) / 4, 256, 1 << 20);
+  bg->deltas.ensure((int64_t)grid + 2);
+  // gather reads the full contribution vector, then the owned slice is
+  // updated in place (stream order keeps the two phases apart)
+  pull_sums(ctx, bg, contrib_dev, nullptr, false, flags, -1, bg->sums.p, true);
+  if (cnt) {
+    ProfScope ps(ctx, 2);
+    k_pr_update<<<grid, 256, 0, ctx->stream>>>(cnt, (1.0 - damping) / (double)bg->n, damping,
+                                               bg->sums.p + v0, ranks_dev + v0, deg_dev + v0,
+                                               contrib_dev + v0, nullptr, bg->deltas.p);
+    after_launch(ctx, "k_pr_update");
+  }
+  if (delta_dev) {
+    if (cnt) {
+      k_reduce_sum<<<1, 1024, 0, ctx->stream>>>(bg->deltas.p, grid, delta_dev);
+      after_launch(ctx, "k_reduce_sum");
+    } else {
+      GCB_CUDA(cudaMemsetAsync(delta_dev, 0, sizeof(double), ctx->stream));
+    }
+  }
+  GCB_API_END
+}
+
 }  // extern "C"

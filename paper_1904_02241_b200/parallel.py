@@ -1,0 +1,235 @@
+"""Multi-GPU TOCAB PageRank: destination-range shards + contribution all-gather.
+
+SURVEY 8e: PageRank shards naturally by destination vertex.  Rank r owns a
+contiguous range [v0_r, v1_r) of the transpose's rows, chosen so every rank
+holds the same number of in-edges (an unpermuted R-MAT is heavily skewed to
+low ids: equal-vertex splits give 1.5-3.5x imbalance, equal-edge splits
+1.000).  Each rank TOCAB-partitions its row slab by source range, keeps the
+full f64 contribution vector, and per iteration
+
+    1. gathers its slab against the full contribution vector (device),
+    2. updates ranks / contributions of its owned slice in place (device),
+    3. all-gathers the owned contribution slices over NCCL (NVLink),
+    4. all-reduces the scalar L1 delta when tol > 0.
+
+One process per GPU; torch.distributed provides the communicator (NCCL on
+B200, gloo for the CPU tests of this module).  ``ShardedPageRank`` is engine-
+agnostic: ``DeviceShard`` runs the sm_100a kernels through the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+import numpy as np
+
+from . import _lib
+from .blocking import BlockedGraph, partition_tocab
+from .graph import CsrGraph
+from .kernels import PrParams, PrResult
+
+__all__ = ["shard_ranges", "DeviceShard", "TorchExchange", "LoopbackExchange",
+           "ShardedPageRank", "sharded_pagerank_virtual"]
+
+
+def shard_ranges(row_offsets, parts: int, align: int = 4) -> np.ndarray:
+    """Split rows into ``parts`` contiguous ranges with ~equal edge counts.
+
+    Boundaries are multiples of ``align`` (the update kernel's vector width)
+    except the last, which is num_rows.  Returns int64[parts + 1]."""
+    ro = np.asarray(row_offsets, dtype=np.int64)
+    n = ro.size - 1
+    if parts < 1:
+        raise ValueError("parts must be >= 1")
+    m = int(ro[-1])
+    cuts = [0]
+    for r in range(1, parts):
+        target = (m * r) // parts
+        v = int(np.searchsorted(ro, target, side="left"))
+        v = min(n, max(cuts[-1], (v // align) * align))
+        cuts.append(v)
+    cuts.append(n)
+    return np.asarray(cuts, dtype=np.int64)
+
+
+@dataclasses.dataclass
+class ShardPlan:
+    ranges: np.ndarray  # int64[P+1]
+
+    @property
+    def parts(self) -> int:
+        return len(self.ranges) - 1
+
+    def owned(self, rank: int) -> tuple[int, int]:
+        return int(self.ranges[rank]), int(self.ranges[rank + 1])
+
+    @property
+    def max_len(self) -> int:
+        return int(np.max(np.diff(self.ranges))) if self.parts else 0
+
+
+class TorchExchange:
+    """All-gather of owned slices with torch.distributed (NCCL or gloo).
+
+    Slices have unequal lengths; each rank packs its slice into a padded send
+    buffer of max_len, ``all_gather_into_tensor`` fills [P, max_len], and the
+    rows are copied back into the full vector."""
+
+    def __init__(self, plan: ShardPlan, rank: int, group=None):
+        self.plan = plan
+        self.rank = rank
+        self.group = group
+        self._buf = {}
+
+    def _buffers(self, full):
+        import torch
+
+        key = (full.device, full.dtype)
+        if key not in self._buf:
+            P, L = self.plan.parts, self.plan.max_len
+            self._buf[key] = (torch.zeros(L, dtype=full.dtype, device=full.device),
+                              torch.zeros(P * L, dtype=full.dtype, device=full.device))
+        return self._buf[key]
+
+    def sync(self, full):
+        import torch.distributed as dist
+
+        send, recv = self._buffers(full)
+        v0, v1 = self.plan.owned(self.rank)
+        send[: v1 - v0].copy_(full[v0:v1])
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+        L = self.plan.max_len
+        for r in range(self.plan.parts):
+            a, b = self.plan.owned(r)
+            if r != self.rank and b > a:
+                full[a:b].copy_(recv[r * L:r * L + (b - a)])
+
+    def allreduce_sum(self, x: float, device) -> float:
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
+
+class LoopbackExchange:
+    """P virtual shards in one process (single-GPU validation of the sharded
+    path): each shard has its own full vectors; sync copies owned slices."""
+
+    def __init__(self, plan: ShardPlan):
+        self.plan = plan
+
+    def sync_all(self, fulls):
+        for r, src in enumerate(fulls):
+            a, b = self.plan.owned(r)
+            for q, dst in enumerate(fulls):
+                if q != r and b > a:
+                    dst[a:b].copy_(src[a:b])
+
+
+class DeviceShard:
+    """One rank's slab of the transpose, TOCAB-blocked, on its GPU."""
+
+    def __init__(self, gt: CsrGraph, v0: int, v1: int, width: int, flags: int = 0):
+        import torch
+
+        h = gt.device()
+        ctx = h.ctx
+        ctx.bind_torch_stream()  # kernels, exchange copies and NCCL share one stream
+        self.ctx = ctx
+        self.n = gt.num_vertices
+        self.v0, self.v1 = int(v0), int(v1)
+        self.flags = int(flags)
+        raw = ctypes.c_void_p()
+        _lib.check(ctx._lib.gcb_csr_row_slab(ctx.handle, h.raw, self.v0, self.v1,
+                                             ctypes.byref(raw)), "row slab")
+        slab = CsrGraph._from_device(ctx, raw)
+        self.m_local = slab.num_edges
+        self.bg: BlockedGraph = partition_tocab(slab, "pull", width)
+        del slab
+        dev = torch.device("cuda", ctx.device)
+        self.deg = torch.empty(self.n, dtype=torch.int32, device=dev)
+        _lib.check(ctx._lib.gcb_csr_col_counts(ctx.handle, h.raw,
+                                               ctypes.c_void_p(self.deg.data_ptr())), "col counts")
+        self.delta = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.device = dev
+
+    def init(self, contrib, ranks):
+        _lib.check(self.ctx._lib.gcb_pr_shard_init(
+            self.ctx.handle, self.bg.device().raw, self.v0, self.v1,
+            ctypes.c_void_p(self.deg.data_ptr()), ctypes.c_void_p(contrib.data_ptr()),
+            ctypes.c_void_p(ranks.data_ptr())), "shard init")
+
+    def step(self, contrib, ranks, damping: float, want_delta: bool):
+        _lib.check(self.ctx._lib.gcb_pr_shard_step(
+            self.ctx.handle, self.bg.device().raw, self.v0, self.v1, float(damping), self.flags,
+            ctypes.c_void_p(self.deg.data_ptr()), ctypes.c_void_p(contrib.data_ptr()),
+            ctypes.c_void_p(ranks.data_ptr()),
+            ctypes.c_void_p(self.delta.data_ptr()) if want_delta else None), "shard step")
+        return self.delta if want_delta else None
+
+
+class ShardedPageRank:
+    """pr_blocked semantics (kernels.py:367-405) across destination shards."""
+
+    def __init__(self, engine, plan: ShardPlan, rank: int, exchange):
+        self.engine = engine
+        self.plan = plan
+        self.rank = rank
+        self.exchange = exchange
+
+    def run(self, params: PrParams = PrParams(), gather_ranks: bool = True) -> PrResult:
+        import torch
+
+        eng = self.engine
+        n = eng.n
+        contrib = torch.zeros(n, dtype=torch.float64, device=eng.device)
+        ranks = torch.zeros(n, dtype=torch.float64, device=eng.device)
+        eng.init(contrib, ranks)
+        self.exchange.sync(contrib)
+        it, conv = 0, False
+        for _ in range(params.max_iters):
+            d = eng.step(contrib, ranks, params.damping, params.tol > 0.0)
+            self.exchange.sync(contrib)
+            it += 1
+            if params.tol > 0.0:
+                total = self.exchange.allreduce_sum(float(d.item()), eng.device)
+                if total < params.tol:
+                    conv = True
+                    break
+        if gather_ranks:
+            self.exchange.sync(ranks)
+        return PrResult(ranks, it, conv)
+
+
+def sharded_pagerank_virtual(gt: CsrGraph, parts: int, width: int,
+                             params: PrParams = PrParams(), exact: bool = False) -> PrResult:
+    """Run ``parts`` destination shards in lockstep on one GPU with loopback
+    exchange -- the single-device check of the multi-GPU algorithm."""
+    import torch
+
+    plan = ShardPlan(shard_ranges(gt.row_offsets, parts))
+    flags = _lib.FLAG_EXACT if exact else 0
+    shards = [DeviceShard(gt, *plan.owned(r), width, flags) for r in range(parts)]
+    n = gt.num_vertices
+    dev = shards[0].device
+    contribs = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(parts)]
+    ranks = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(parts)]
+    ex = LoopbackExchange(plan)
+    for s, c, r in zip(shards, contribs, ranks):
+        s.init(c, r)
+    ex.sync_all(contribs)
+    it, conv = 0, False
+    for _ in range(params.max_iters):
+        deltas = [s.step(c, r, params.damping, params.tol > 0.0)
+                  for s, c, r in zip(shards, contribs, ranks)]
+        ex.sync_all(contribs)
+        it += 1
+        if params.tol > 0.0 and sum(float(d.item()) for d in deltas) < params.tol:
+            conv = True
+            break
+    ex.sync_all(ranks)
+    torch.cuda.synchronize(dev)
+    return PrResult(ranks[0].cpu().numpy(), it, conv)
