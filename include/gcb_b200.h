@@ -52,6 +52,7 @@ extern "C" {
 #define GCB_FLAG_F32_VALUES 2u   /* f32 copy of the gathered vector (f64 sums) */
 #define GCB_FLAG_NO_L2_WINDOW 4u /* disable the per-block access-policy window */
 #define GCB_FLAG_NO_GRAPH 8u     /* launch eagerly instead of a CUDA graph     */
+#define GCB_FLAG_NO_RELABEL 16u  /* fast pull paths: keep the input numbering  */
 
 /* BFS direction modes (DirectionPolicy.MODES, traversal.py:46-61) */
 #define GCB_BFS_AUTO 0

@@ -217,6 +217,187 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
   }  // t < ntiles
 }
 
+// ---------------------------------------------------------------------------
+// k_pull_prefix: the gather for the degree-ordered layout (relabel.cu).
+//
+// ncu (profiles/r1b_*) put the hot-staged kernel at the L1TEX sector ceiling
+// (~0.9 global sectors per SM cycle; a pure random-gather microbenchmark tops
+// out at 0.95, scripts/mb_gather.cu), so every change here removes sectors or
+// instructions:
+//   * hot table = the block's first H sources (the hottest, by construction)
+//     copied contiguously into shared memory: no recoded arena, no fill pass;
+//   * col_idx streamed with one 256-bit load per lane (8 edges = one full
+//     32-byte sector; the two 128-bit loads it replaces touched 2 sectors);
+//   * row boundaries come from a 1-bit-per-edge row-start bitmap (32 bytes per
+//     256-edge tile, one sector per warp) instead of lro tables + a binary
+//     search in shared memory.  Local rows are never empty (blocking.py:
+//     189-201), so row(q) = tile_row + #row starts in (first, q].
+// Reduction and emission are as in k_gather: in-lane runs, a segmented
+// shuffle scan over lane tails, plain read-modify-write for rows inside the
+// tile and f64 RED for rows that cross a tile boundary.
+// ---------------------------------------------------------------------------
+// ASSIGN: out is all zero before this launch (first block of the pass), so a
+// row that lies inside one tile is stored (out[v] = x) instead of
+// read-modify-written -- no dependent load on the emit path.
+template <bool WGT, bool ASSIGN>
+__global__ void __launch_bounds__(kGWarps * 32, 1)
+    k_pull_prefix(const uint32_t *__restrict__ col, const double *__restrict__ w,
+                  const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ id_map_b,
+                  const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
+                  int64_t ntiles, uint32_t lo, int hot, uint32_t Lb,
+                  const double *__restrict__ vals, double *__restrict__ out) {
+  constexpr int V = kTileV;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // per-warp cache of the destination ids of the tile's first 32 rows
+  uint32_t *s_ids = reinterpret_cast<uint32_t *>(smem) + wid * 32;
+  double *s_hot = reinterpret_cast<double *>(smem + kGWarps * 32 * sizeof(uint32_t));
+  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+  const unsigned FULL = 0xffffffffu;
+  const int64_t stride = (int64_t)gridDim.x * kGWarps;
+
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) s_hot[i] = __ldcg(vals + lo + i);
+  __syncthreads();
+
+  int64_t t = (int64_t)blockIdx.x * kGWarps + wid;
+  if (t >= ntiles) return;
+  // software pipeline: tile t's col chunk, bitmap words and first row
+  uint32_t c[V], fw, r0, idl;
+  {
+    const int64_t abase = (t0 + t) * kTileT;
+    ld_stream_u32x8(col + abase + lane * V, pol_stream, c);
+    fw = rstart[(abase >> 5) + (lane < 8 ? lane : 8)];
+    r0 = tile_row[t];
+    idl = r0 + lane < Lb ? id_map_b[r0 + lane] : 0u;
+  }
+  for (; t < ntiles; t += stride) {
+    const int64_t abase = (t0 + t) * kTileT;
+    const int64_t tn = t + stride;
+    uint32_t cn[V] = {0, 0, 0, 0, 0, 0, 0, 0}, fwn = 0, r0n = 0;
+    if (tn < ntiles) {
+      const int64_t nb = (t0 + tn) * kTileT;
+      ld_stream_u32x8(col + nb + lane * V, pol_stream, cn);
+      fwn = rstart[(nb >> 5) + (lane < 8 ? lane : 8)];
+      r0n = tile_row[tn];
+    }
+    s_ids[lane] = idl;
+    // valid tile positions [llo, lhi)
+    const int llo = es > abase ? (int)(es - abase) : 0;
+    const int lhi = ee - abase < kTileT ? (int)(ee - abase) : kTileT;
+    const int p0 = lane * V;
+
+    // gathers (issued first: everything below overlaps their latency)
+    double v[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const uint32_t h = c[k] - lo;
+      double x;
+      if (h < (uint32_t)hot) x = s_hot[h];
+      else x = ld_keep(vals + c[k], pol_keep);
+      v[k] = x;
+    }
+    if (WGT) {
+      double ww[V];
+      ld_stream_f64x4(w + abase + p0, pol_stream, ww);
+      ld_stream_f64x4(w + abase + p0 + 4, pol_stream, ww + 4);
+#pragma unroll
+      for (int k = 0; k < V; ++k) v[k] = __dmul_rn(ww[k], v[k]);
+    }
+
+    // row-start bits of this lane's 8 edges, restricted to valid positions;
+    // the bit of the tile's first valid edge is dropped (its row is r0)
+    const uint32_t wl = __shfl_sync(FULL, fw, lane >> 2);
+    uint32_t bits = (wl >> ((lane & 3) * 8)) & 0xffu;
+    const int a = llo - p0, z = lhi - p0;  // valid k in [a, z)
+    const uint32_t vm = (z <= 0 || a >= V) ? 0u
+                        : ((0xffu >> (V - (z < V ? z : V))) & (0xffu << (a > 0 ? a : 0)));
+    const uint32_t first_word = __shfl_sync(FULL, fw, llo >> 5);
+    const bool first_start = (first_word >> (llo & 31)) & 1u;
+    const bool last_cont = (lhi == kTileT) && !(__shfl_sync(FULL, fw, 8) & 1u);
+    if (a >= 0 && a < V) bits &= ~(1u << a);
+    bits &= vm;
+    // exclusive prefix of row starts over lanes
+    const int cnt = __popc(bits);
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const uint32_t r_last = r0 + (uint32_t)__shfl_sync(FULL, incl, 31);
+    const bool lane_valid = vm != 0;
+    const int kf = lane_valid ? __ffs(vm) - 1 : 0;
+    uint32_t j = r0 + (uint32_t)(incl - cnt) + ((bits >> kf) & 1u);
+
+    // next tile's id cache (its first row is known; overlaps the reduction)
+    uint32_t idn = 0;
+    if (tn < ntiles && r0n + lane < Lb) idn = id_map_b[r0n + lane];
+    __syncwarp();
+    auto emit = [&](uint32_t row, double x) {
+      const uint32_t rr = row - r0;
+      const uint32_t vid = rr < 32 ? s_ids[rr] : id_map_b[row];
+      if ((row == r0 && !first_start) || (row == r_last && last_cont)) atomicAdd(out + vid, x);
+      else if (ASSIGN) out[vid] = x;
+      else out[vid] = __dadd_rn(out[vid], x);
+    };
+
+    const uint32_t head_j = j;
+    double head_sum = 0.0, acc = 0.0;
+    bool head_closed = false;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      if (!((vm >> k) & 1u)) continue;
+      if (k > kf && ((bits >> k) & 1u)) {
+        if (j == head_j && !head_closed) {
+          head_sum = acc;
+          head_closed = true;
+        } else {
+          emit(j, acc);
+        }
+        acc = 0.0;
+        ++j;
+      }
+      acc = __dadd_rn(acc, v[k]);
+    }
+    // segmented inclusive scan of the lane tails (key = tail row)
+    int key = lane_valid ? (int)j : -1 - lane;
+    double val = acc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int k2 = __shfl_up_sync(FULL, key, d);
+      const double v2 = __shfl_up_sync(FULL, val, d);
+      if (lane >= d && k2 == key) val = __dadd_rn(v2, val);
+    }
+    int pk = __shfl_up_sync(FULL, key, 1);
+    const double pv = __shfl_up_sync(FULL, val, 1);
+    if (lane == 0) pk = -1000;
+    int nh = __shfl_down_sync(FULL, lane_valid ? (int)head_j : -1000, 1);
+    if (lane == 31) nh = -1000;
+    if (lane_valid) {
+      if (head_closed) emit(head_j, (pk == (int)head_j) ? __dadd_rn(pv, head_sum) : head_sum);
+      if (nh != (int)j) emit(j, val);
+    }
+    // rotate the pipeline
+#pragma unroll
+    for (int k = 0; k < V; ++k) c[k] = cn[k];
+    fw = fwn;
+    r0 = r0n;
+    idl = idn;
+    __syncwarp();
+  }
+}
+
+// rstart bit q = arena edge q is the first edge of its local row; bit m is a
+// sentinel (set) so the last tile of the last block sees its row closed.
+__global__ void k_row_start_bits(int64_t Lb, int64_t es, const uint32_t *__restrict__ lro_b,
+                                 uint32_t *__restrict__ bits) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= Lb;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = es + lro_b[r];
+    atomicOr(bits + (q >> 5), 1u << (q & 31));
+  }
+}
+
 // hotval[b][s] = vals[hot_ids[b][s]]
 __global__ void k_fill_hot(int64_t count, const uint32_t *__restrict__ ids,
                            const double *__restrict__ vals, double *__restrict__ hotval) {
@@ -351,10 +532,79 @@ static void fill_hot(gcb_ctx *ctx, gcb_blocked *bg, const double *vals) {
   after_launch(ctx, "k_fill_hot");
 }
 
+// ---- degree-ordered layout: row-start bitmap + prefix hot table ----
+static int64_t prefix_hot_slots(gcb_ctx *ctx) {
+  int optin = 0;
+  GCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  int64_t K = ((int64_t)optin - 1024 - kGWarps * 128) / 8;
+  const char *env = getenv("GCB_HOT_K");
+  // 16K slots (128 KB): measured best at scale 24 -- a larger table takes the
+  // L1 capacity the cold misses are staged in (scripts/mb_gather.cu: random
+  // LDG rate 0.93 / 0.86 / 0.50 per SM cycle with 0 / 128 / 192 KB of smem)
+  int64_t want = env ? atoll(env) : 16384;
+  if (want < K) K = want;
+  return K < 0 ? 0 : K;
+}
+
+static void ensure_prefix_exec(gcb_ctx *ctx, gcb_blocked *bg) {
+  ensure_derived(ctx, bg);
+  if (bg->rready) return;
+  const int64_t words = (bg->m + kColPad) / 32 + 16;
+  bg->rstart.alloc(words);
+  GCB_CUDA(cudaMemsetAsync(bg->rstart.p, 0, words * sizeof(uint32_t), ctx->stream));
+  for (int64_t b = 0; b < bg->B; ++b) {
+    const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+    if (Lb == 0) continue;
+    k_row_start_bits<<<grid_for(Lb + 1, 256, 65536), 256, 0, ctx->stream>>>(
+        Lb, bg->h_edge_starts[b], bg->lro.p + rs + b, bg->rstart.p);
+    after_launch(ctx, "k_row_start_bits");
+  }
+  bg->hot_k = prefix_hot_slots(ctx);
+  sync(ctx);
+  bg->rready = true;
+}
+
+template <bool WGT, bool ASSIGN>
+static void launch_prefix(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double *vals, double *out) {
+  const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+  const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
+  const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
+  const int64_t lo = b * bg->width, hi = (lo + bg->width < bg->n) ? lo + bg->width : bg->n;
+  const int hot = (int)(bg->hot_k < hi - lo ? bg->hot_k : hi - lo);
+  const size_t smem = (size_t)hot * 8 + kGWarps * 32 * sizeof(uint32_t);
+  static size_t done = 0;
+  if (smem > done) {
+    GCB_CUDA(cudaFuncSetAttribute(k_pull_prefix<WGT, ASSIGN>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done = smem;
+  }
+  int64_t grid = ceil_div(nt, kGWarps);
+  if (grid > ctx->num_sms) grid = ctx->num_sms;
+  k_pull_prefix<WGT, ASSIGN><<<(unsigned)(grid < 1 ? 1 : grid), kGWarps * 32, smem, ctx->stream>>>(
+      bg->col.p, WGT ? bg->w.p : nullptr, bg->rstart.p, bg->id_map.p + rs, bg->tile_row.p + tb, es,
+      ee, bg->h_tile_t0[b], nt, (uint32_t)lo, hot, (uint32_t)Lb, vals, out);
+  after_launch(ctx, "k_pull_prefix");
+}
+
 // out[v] += sum over the rows of v in every block (block order); the caller
 // clears out first.
 void gather_accum(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights,
                   uint32_t flags, double *out) {
+  if (bg->is_relabeled && getenv("GCB_OLD_PREFIX") == nullptr) {
+    ensure_prefix_exec(ctx, bg);
+    const bool wgt = use_weights && bg->weighted;
+    bool first = true;  // out is zero before the first launch (callers clear it)
+    for (int64_t b = 0; b < bg->B; ++b) {
+      if (bg->h_row_starts[b + 1] == bg->h_row_starts[b]) continue;
+      ProfScope ps(ctx, 0);
+      if (wgt && first) launch_prefix<true, true>(ctx, bg, b, vals, out);
+      else if (wgt) launch_prefix<true, false>(ctx, bg, b, vals, out);
+      else if (first) launch_prefix<false, true>(ctx, bg, b, vals, out);
+      else launch_prefix<false, false>(ctx, bg, b, vals, out);
+      first = false;
+    }
+    return;
+  }
   ensure_exec(ctx, bg);
   const bool wgt = use_weights && bg->weighted;
   const bool hot = bg->hot_k > 0;

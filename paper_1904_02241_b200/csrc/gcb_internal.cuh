@@ -163,6 +163,9 @@ struct gcb_blocked {
   gcb::DArray<uint32_t> xcol;        // col arena recoded: 0x80000000|slot for hot sources
   gcb::DArray<uint32_t> hot_ids;     // [B][hot_k] source id of each slot (or ~0u)
   gcb::DArray<double> hotval;        // [B][hot_k] staged values for the next gather
+  // degree-ordered copies (is_relabeled): row-start bitmap of the arena
+  bool rready = false;
+  gcb::DArray<uint32_t> rstart;      // bit q: arena edge q starts a local row
 
   // ---- workspaces (grown on demand) ----
   gcb::DArray<double> partials;  // [L]
@@ -172,6 +175,16 @@ struct gcb_blocked {
   gcb::DArray<double> sums;      // [n] (push)
   gcb::DArray<double> deltas;    // [R + 1]
   gcb::DArray<double> ranks;     // [n]
+
+  // ---- degree-ordered execution copy of a pull graph (relabel.cu) ----
+  bool is_relabeled = false;         // this object is such a copy
+  gcb_blocked *rl = nullptr;         // the copy (owned), built on first fast call
+  gcb::DArray<uint32_t> rl_perm;     // [n] original id -> renumbered id
+
+  gcb_blocked() = default;
+  gcb_blocked(const gcb_blocked &) = delete;
+  gcb_blocked &operator=(const gcb_blocked &) = delete;
+  ~gcb_blocked();
 };
 
 namespace gcb {
@@ -266,6 +279,11 @@ void cub_sort_pairs_desc_u32_u32(gcb_ctx *ctx, uint32_t *keys, uint32_t *keys_al
                                  uint32_t **res_vals);
 void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sums,
                   bool use_weights, uint32_t flags, int64_t block_only);
+// relabel.cu: degree-ordered execution copy of a pull graph
+bool relabel_enabled(const gcb_blocked *bg, uint32_t flags);
+gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg);
+void permute_in(gcb_ctx *ctx, const gcb_blocked *bg, const double *x, double *x_new);
+void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, double *y);
 // cub wrappers (cub_ops.cu)
 void cub_sort_keys_u64(gcb_ctx *ctx, uint64_t *keys, uint64_t *keys_alt, int64_t m, int end_bit,
                        uint64_t **result);

@@ -33,6 +33,18 @@ __device__ __forceinline__ double2 ld_stream_d2(const void *ptr, uint64_t pol) {
       : "l"(ptr), "l"(pol));
   return r;
 }
+// 256-bit loads (sm_100+: LDG.E.256): one full 32-byte sector per lane
+__device__ __forceinline__ void ld_stream_u32x8(const void *ptr, uint64_t pol, uint32_t (&c)[8]) {
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+      : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]),
+        "=r"(c[7])
+      : "l"(ptr), "l"(pol));
+}
+__device__ __forceinline__ void ld_stream_f64x4(const void *ptr, uint64_t pol, double *d) {
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+      : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3])
+      : "l"(ptr), "l"(pol));
+}
 __device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
   double r;
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));

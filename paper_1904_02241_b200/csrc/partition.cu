@@ -289,6 +289,12 @@ void compute_range_bounds(gcb_ctx *ctx, const gcb_blocked *bg, int64_t k, int64_
   after_launch(ctx, "k_range_bounds");
 }
 
+}  // namespace gcb
+
+gcb_blocked::~gcb_blocked() { delete rl; }
+
+namespace gcb {
+
 void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
   if (bg->derived) return;
   int64_t n = bg->n, B = bg->B;

@@ -631,6 +631,14 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   const int64_t n = bg->n;
   const bool exact = flags & GCB_FLAG_EXACT;
   const bool push = bg->direction == 1;
+  if (!(flags & GCB_FLAG_F32_VALUES) && !deg_override && relabel_enabled(bg, flags)) {
+    // run on the degree-ordered copy (relabel.cu); ranks come back in input order
+    gcb_blocked *rl = ensure_relabeled(ctx, bg);
+    rl->ranks.ensure(n);
+    pr_run(ctx, rl, damping, tol, max_iters, flags, nullptr, rl->ranks.p, iters, conv);
+    permute_out(ctx, bg, rl->ranks.p, ranks_dev);
+    return;
+  }
   const bool f32 = (flags & GCB_FLAG_F32_VALUES) && !exact && !push;
   const uint32_t *deg = deg_override ? deg_override : bg->deg.p;
   bg->contrib.ensure(n);
@@ -830,6 +838,15 @@ int gcb_accumulate_ranges(gcb_ctx *ctx, gcb_blocked *bg, const double *partials_
 // y = pull gather of x over a blocking, accumulated block by block
 static void pull_spmv(gcb_ctx *ctx, gcb_blocked *bg, const double *x, bool weights, uint32_t flags,
                       double *y) {
+  if (bg->n > 0 && relabel_enabled(bg, flags)) {
+    gcb_blocked *rl = ensure_relabeled(ctx, bg);
+    rl->contrib.ensure(bg->n);
+    rl->sums.ensure(bg->n);
+    permute_in(ctx, bg, x, rl->contrib.p);
+    pull_spmv(ctx, rl, rl->contrib.p, weights, flags, rl->sums.p);
+    permute_out(ctx, bg, rl->sums.p, y);
+    return;
+  }
   GCB_CUDA(cudaMemsetAsync(y, 0, (bg->n ? bg->n : 1) * sizeof(double), ctx->stream));
   pull_sums(ctx, bg, x, nullptr, weights, flags, -1, y, true);
 }
