@@ -2,6 +2,8 @@
 #include <cstdarg>
 #include <cstring>
 
+#include <cstdlib>
+
 #include "gcb_internal.cuh"
 
 namespace gcb {
@@ -69,9 +71,12 @@ int gcb_ctx_create(int device, gcb_ctx **out) {
     delete ctx;
     GCB_CUDA(e);
   }
-  // Reserve the persisting L2 set-aside once per context: the per-block
-  // access-policy windows of the pull gather land in it (north star (1)).
-  if (ctx->persist_max > 0) {
+  // Persisting L2 set-aside (for access-policy windows): opt-in only.
+  // Measured at scale 24 it slows every pass -- the rank update went from
+  // 0.12 to 0.24 ms per iteration and the gather from 0.92 to 1.00 ms -- while
+  // per-load L2::evict_last hints (createpolicy, ldst.cuh) keep the block's
+  // value slice resident without carving L2 (profiles/r1b_l2_policy.txt).
+  if (ctx->persist_max > 0 && getenv("GCB_L2_PERSIST")) {
     cudaError_t le = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)ctx->persist_max);
     if (le != cudaSuccess) (void)cudaGetLastError();
   }

@@ -239,27 +239,27 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
 // ASSIGN: out is all zero before this launch (first block of the pass), so a
 // row that lies inside one tile is stored (out[v] = x) instead of
 // read-modify-written -- no dependent load on the emit path.
-template <bool WGT, bool ASSIGN>
-__global__ void __launch_bounds__(kGWarps * 32, 1)
+template <bool WGT, bool ASSIGN, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
     k_pull_prefix(const uint32_t *__restrict__ col, const double *__restrict__ w,
                   const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ id_map_b,
                   const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
-                  int64_t ntiles, uint32_t lo, int hot, uint32_t Lb,
+                  int64_t ntiles, uint32_t lo, int hot, uint32_t warm, uint32_t Lb, int l2hint,
                   const double *__restrict__ vals, double *__restrict__ out) {
   constexpr int V = kTileV;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // per-warp cache of the destination ids of the tile's first 32 rows
   uint32_t *s_ids = reinterpret_cast<uint32_t *>(smem) + wid * 32;
-  double *s_hot = reinterpret_cast<double *>(smem + kGWarps * 32 * sizeof(uint32_t));
-  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+  double *s_hot = reinterpret_cast<double *>(smem + NW * 32 * sizeof(uint32_t));
+  const uint64_t pol_stream = policy_evict_first(), pol_keep = l2hint == 0 ? policy_evict_last() : l2hint == 1 ? policy_evict_normal() : policy_evict_first();
   const unsigned FULL = 0xffffffffu;
-  const int64_t stride = (int64_t)gridDim.x * kGWarps;
+  const int64_t stride = (int64_t)gridDim.x * NW;
 
   for (int i = threadIdx.x; i < hot; i += blockDim.x) s_hot[i] = __ldcg(vals + lo + i);
   __syncthreads();
 
-  int64_t t = (int64_t)blockIdx.x * kGWarps + wid;
+  int64_t t = (int64_t)blockIdx.x * NW + wid;
   if (t >= ntiles) return;
   // software pipeline: tile t's col chunk, bitmap words and first row
   uint32_t c[V], fw, r0, idl;
@@ -293,7 +293,8 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
       const uint32_t h = c[k] - lo;
       double x;
       if (h < (uint32_t)hot) x = s_hot[h];
-      else x = ld_keep(vals + c[k], pol_keep);
+      else if (h < warm) x = ld_warm(vals + c[k], pol_keep);
+      else x = ld_cold(vals + c[k], pol_keep);
       v[k] = x;
     }
     if (WGT) {
@@ -533,17 +534,29 @@ static void fill_hot(gcb_ctx *ctx, gcb_blocked *bg, const double *vals) {
 }
 
 // ---- degree-ordered layout: row-start bitmap + prefix hot table ----
-static int64_t prefix_hot_slots(gcb_ctx *ctx) {
+// Shared-memory carve-out of the prefix gather (KB; one of the sm_100
+// configurations) and the hot slots that fill it.  The rest of the 256 KB
+// unified array is L1, where the warm tier lives and the cold misses are
+// staged: a larger table starves them (scripts/mb_gather.cu: random LDG at
+// 0.93 / 0.86 / 0.50 per SM cycle with 0 / 128 / 192 KB of shared memory).
+static int prefix_carveout_kb() {
+  const char *env = getenv("GCB_CARVE_KB");
+  return env ? atoi(env) : 132;
+}
+static int64_t prefix_hot_slots(gcb_ctx *ctx, int nw) {
   int optin = 0;
   GCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  int64_t K = ((int64_t)optin - 1024 - kGWarps * 128) / 8;
+  int64_t budget = (int64_t)prefix_carveout_kb() * 1024;
+  if (budget > optin + 1024) budget = optin + 1024;
+  // 1 KB per CTA is reserved by the system; the id caches take kGWarps * 128 B
+  int64_t K = (budget - 1024 - (int64_t)nw * 128) / 8;
   const char *env = getenv("GCB_HOT_K");
-  // 16K slots (128 KB): measured best at scale 24 -- a larger table takes the
-  // L1 capacity the cold misses are staged in (scripts/mb_gather.cu: random
-  // LDG rate 0.93 / 0.86 / 0.50 per SM cycle with 0 / 128 / 192 KB of smem)
-  int64_t want = env ? atoll(env) : 16384;
-  if (want < K) K = want;
+  if (env && atoll(env) < K) K = atoll(env);
   return K < 0 ? 0 : K;
+}
+static uint32_t prefix_warm_end(int64_t hot) {
+  const char *env = getenv("GCB_WARM");
+  return env ? (uint32_t)atoll(env) : (uint32_t)(hot + 16384);
 }
 
 static void ensure_prefix_exec(gcb_ctx *ctx, gcb_blocked *bg) {
@@ -559,31 +572,51 @@ static void ensure_prefix_exec(gcb_ctx *ctx, gcb_blocked *bg) {
         Lb, bg->h_edge_starts[b], bg->lro.p + rs + b, bg->rstart.p);
     after_launch(ctx, "k_row_start_bits");
   }
-  bg->hot_k = prefix_hot_slots(ctx);
   sync(ctx);
   bg->rready = true;
 }
 
-template <bool WGT, bool ASSIGN>
-static void launch_prefix(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double *vals, double *out) {
+template <bool WGT, bool ASSIGN, int NW>
+static void launch_prefix_nw(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double *vals,
+                             double *out) {
   const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
   const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
   const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
   const int64_t lo = b * bg->width, hi = (lo + bg->width < bg->n) ? lo + bg->width : bg->n;
-  const int hot = (int)(bg->hot_k < hi - lo ? bg->hot_k : hi - lo);
-  const size_t smem = (size_t)hot * 8 + kGWarps * 32 * sizeof(uint32_t);
+  const int64_t hot_cap = prefix_hot_slots(ctx, NW);
+  const int hot = (int)(hot_cap < hi - lo ? hot_cap : hi - lo);
+  const size_t smem = (size_t)hot * 8 + NW * 32 * sizeof(uint32_t);
   static size_t done = 0;
   if (smem > done) {
-    GCB_CUDA(cudaFuncSetAttribute(k_pull_prefix<WGT, ASSIGN>,
+    GCB_CUDA(cudaFuncSetAttribute(k_pull_prefix<WGT, ASSIGN, NW>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int pct = (int)(100.0 * prefix_carveout_kb() / 228.0 + 0.99);
+    if (pct > 100) pct = 100;
+    GCB_CUDA(cudaFuncSetAttribute(k_pull_prefix<WGT, ASSIGN, NW>,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     done = smem;
   }
-  int64_t grid = ceil_div(nt, kGWarps);
+  int64_t grid = ceil_div(nt, NW);
   if (grid > ctx->num_sms) grid = ctx->num_sms;
-  k_pull_prefix<WGT, ASSIGN><<<(unsigned)(grid < 1 ? 1 : grid), kGWarps * 32, smem, ctx->stream>>>(
+  k_pull_prefix<WGT, ASSIGN, NW><<<(unsigned)(grid < 1 ? 1 : grid), NW * 32, smem, ctx->stream>>>(
       bg->col.p, WGT ? bg->w.p : nullptr, bg->rstart.p, bg->id_map.p + rs, bg->tile_row.p + tb, es,
-      ee, bg->h_tile_t0[b], nt, (uint32_t)lo, hot, (uint32_t)Lb, vals, out);
+      ee, bg->h_tile_t0[b], nt, (uint32_t)lo, hot, prefix_warm_end(hot), (uint32_t)Lb,
+      getenv("GCB_L2HINT") ? atoi(getenv("GCB_L2HINT")) : 0, vals, out);
   after_launch(ctx, "k_pull_prefix");
+}
+
+static int prefix_warps() {
+  const char *env = getenv("GCB_PWARPS");
+  return env ? atoi(env) : 32;
+}
+
+template <bool WGT, bool ASSIGN>
+static void launch_prefix(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double *vals, double *out) {
+  switch (prefix_warps()) {
+    case 16: launch_prefix_nw<WGT, ASSIGN, 16>(ctx, bg, b, vals, out); break;
+    case 24: launch_prefix_nw<WGT, ASSIGN, 24>(ctx, bg, b, vals, out); break;
+    default: launch_prefix_nw<WGT, ASSIGN, 32>(ctx, bg, b, vals, out); break;
+  }
 }
 
 // out[v] += sum over the rows of v in every block (block order); the caller

@@ -19,6 +19,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint4 ld_stream_u4(const void *ptr, uint64_t pol) {
   uint4 r;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
@@ -45,9 +50,31 @@ __device__ __forceinline__ void ld_stream_f64x4(const void *ptr, uint64_t pol, d
       : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3])
       : "l"(ptr), "l"(pol));
 }
+// read-write streams (the same thread stores the line back): no .nc
+__device__ __forceinline__ void ld_rw_f64x4(const double *ptr, double *d) {
+  asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3])
+               : "l"(ptr));
+}
+__device__ __forceinline__ void st_f64x4(double *ptr, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
 __device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
   double r;
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+// L1 tiers for the degree-ordered gather: warm sources stay in L1, cold ones
+// do not displace them
+__device__ __forceinline__ double ld_warm(const double *p, uint64_t pol) {
+  double r;
+  asm("ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_cold(const double *p, uint64_t pol) {
+  double r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
   return r;
 }
 __device__ __forceinline__ double ld_keep(const float *p, uint64_t pol) {
