@@ -236,6 +236,23 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
 // shuffle scan over lane tails, plain read-modify-write for rows inside the
 // tile and f64 RED for rows that cross a tile boundary.
 // ---------------------------------------------------------------------------
+// One source value: the block's hot prefix from shared memory, everything
+// else from L2 (evict_last keeps the block's value slice resident; no L1
+// allocation, cold lines would only evict each other).  Predicated loads, no
+// branch: the compiler's if/else cost a BSSY/BSYNC pair per edge.
+__device__ __forceinline__ double gather_one(const double *vals, uint32_t c, uint32_t lo,
+                                             uint32_t hot, uint32_t s_hot, uint64_t pol) {
+  const uint32_t h = c - lo;
+  double x;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.lt.u32 p, %1, %2;\n\t"
+      "@p ld.shared.f64 %0, [%3];\n\t"
+      "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%4], %5;\n\t}"
+      : "=d"(x)
+      : "r"(h), "r"(hot), "r"(s_hot + h * 8u), "l"(vals + c), "l"(pol));
+  return x;
+}
+
 // ASSIGN: out is all zero before this launch (first block of the pass), so a
 // row that lies inside one tile is stored (out[v] = x) instead of
 // read-modify-written -- no dependent load on the emit path.
@@ -244,7 +261,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     k_pull_prefix(const uint32_t *__restrict__ col, const double *__restrict__ w,
                   const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ id_map_b,
                   const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
-                  int64_t ntiles, uint32_t lo, int hot, uint32_t warm, uint32_t Lb, int l2hint,
+                  int64_t ntiles, uint32_t lo, int hot, uint32_t Lb,
                   const double *__restrict__ vals, double *__restrict__ out) {
   constexpr int V = kTileV;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -252,7 +269,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
   // per-warp cache of the destination ids of the tile's first 32 rows
   uint32_t *s_ids = reinterpret_cast<uint32_t *>(smem) + wid * 32;
   double *s_hot = reinterpret_cast<double *>(smem + NW * 32 * sizeof(uint32_t));
-  const uint64_t pol_stream = policy_evict_first(), pol_keep = l2hint == 0 ? policy_evict_last() : l2hint == 1 ? policy_evict_normal() : policy_evict_first();
+  const uint32_t s_hot_addr = (uint32_t)__cvta_generic_to_shared(s_hot);
+  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
   const unsigned FULL = 0xffffffffu;
   const int64_t stride = (int64_t)gridDim.x * NW;
 
@@ -261,7 +279,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 
   int64_t t = (int64_t)blockIdx.x * NW + wid;
   if (t >= ntiles) return;
-  // software pipeline: tile t's col chunk, bitmap words and first row
+  // software pipeline: tile t's col chunk, bitmap words, first row and its ids
   uint32_t c[V], fw, r0, idl;
   {
     const int64_t abase = (t0 + t) * kTileT;
@@ -273,110 +291,116 @@ __global__ void __launch_bounds__(NW * 32, 1)
   for (; t < ntiles; t += stride) {
     const int64_t abase = (t0 + t) * kTileT;
     const int64_t tn = t + stride;
+    const bool has_next = tn < ntiles;
     uint32_t cn[V] = {0, 0, 0, 0, 0, 0, 0, 0}, fwn = 0, r0n = 0;
-    if (tn < ntiles) {
+    if (has_next) {
       const int64_t nb = (t0 + tn) * kTileT;
       ld_stream_u32x8(col + nb + lane * V, pol_stream, cn);
       fwn = rstart[(nb >> 5) + (lane < 8 ? lane : 8)];
       r0n = tile_row[tn];
     }
-    s_ids[lane] = idl;
-    // valid tile positions [llo, lhi)
-    const int llo = es > abase ? (int)(es - abase) : 0;
-    const int lhi = ee - abase < kTileT ? (int)(ee - abase) : kTileT;
-    const int p0 = lane * V;
-
-    // gathers (issued first: everything below overlaps their latency)
+    // gathers first: everything below overlaps their latency
     double v[V];
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const uint32_t h = c[k] - lo;
-      double x;
-      if (h < (uint32_t)hot) x = s_hot[h];
-      else if (h < warm) x = ld_warm(vals + c[k], pol_keep);
-      else x = ld_cold(vals + c[k], pol_keep);
-      v[k] = x;
-    }
+    for (int k = 0; k < V; ++k) v[k] = gather_one(vals, c[k], lo, (uint32_t)hot, s_hot_addr, pol_keep);
     if (WGT) {
       double ww[V];
-      ld_stream_f64x4(w + abase + p0, pol_stream, ww);
-      ld_stream_f64x4(w + abase + p0 + 4, pol_stream, ww + 4);
+      ld_stream_f64x4(w + abase + lane * V, pol_stream, ww);
+      ld_stream_f64x4(w + abase + lane * V + 4, pol_stream, ww + 4);
 #pragma unroll
       for (int k = 0; k < V; ++k) v[k] = __dmul_rn(ww[k], v[k]);
     }
-
-    // row-start bits of this lane's 8 edges, restricted to valid positions;
-    // the bit of the tile's first valid edge is dropped (its row is r0)
-    const uint32_t wl = __shfl_sync(FULL, fw, lane >> 2);
-    uint32_t bits = (wl >> ((lane & 3) * 8)) & 0xffu;
-    const int a = llo - p0, z = lhi - p0;  // valid k in [a, z)
+    // valid tile positions [llo, lhi); lane's valid k in [a, z)
+    const int llo = es > abase ? (int)(es - abase) : 0;
+    const int lhi = ee - abase < kTileT ? (int)(ee - abase) : kTileT;
+    const int a = llo - lane * V, z = lhi - lane * V;
     const uint32_t vm = (z <= 0 || a >= V) ? 0u
                         : ((0xffu >> (V - (z < V ? z : V))) & (0xffu << (a > 0 ? a : 0)));
-    const uint32_t first_word = __shfl_sync(FULL, fw, llo >> 5);
-    const bool first_start = (first_word >> (llo & 31)) & 1u;
-    const bool last_cont = (lhi == kTileT) && !(__shfl_sync(FULL, fw, 8) & 1u);
+    // row-start bits of the lane's edges (valid ones; the tile's first valid
+    // edge dropped -- its row is r0)
+    const uint32_t wl = __shfl_sync(FULL, fw, lane >> 2);
+    uint32_t bits = (wl >> ((lane & 3) * 8)) & vm;
     if (a >= 0 && a < V) bits &= ~(1u << a);
-    bits &= vm;
-    // exclusive prefix of row starts over lanes
-    const int cnt = __popc(bits);
-    int incl = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, d);
-      if (lane >= d) incl += y;
-    }
-    const uint32_t r_last = r0 + (uint32_t)__shfl_sync(FULL, incl, 31);
-    const bool lane_valid = vm != 0;
-    const int kf = lane_valid ? __ffs(vm) - 1 : 0;
-    uint32_t j = r0 + (uint32_t)(incl - cnt) + ((bits >> kf) & 1u);
-
-    // next tile's id cache (its first row is known; overlaps the reduction)
+    const bool first_start = (__shfl_sync(FULL, fw, llo >> 5) >> (llo & 31)) & 1u;
+    const bool last_cont = (lhi == kTileT) && !(__shfl_sync(FULL, fw, 8) & 1u);
+    // next tile's id cache (its first row is known by now)
     uint32_t idn = 0;
-    if (tn < ntiles && r0n + lane < Lb) idn = id_map_b[r0n + lane];
-    __syncwarp();
-    auto emit = [&](uint32_t row, double x) {
-      const uint32_t rr = row - r0;
-      const uint32_t vid = rr < 32 ? s_ids[rr] : id_map_b[row];
-      if ((row == r0 && !first_start) || (row == r_last && last_cont)) atomicAdd(out + vid, x);
-      else if (ASSIGN) out[vid] = x;
-      else out[vid] = __dadd_rn(out[vid], x);
-    };
+    if (has_next && r0n + lane < Lb) idn = id_map_b[r0n + lane];
 
-    const uint32_t head_j = j;
-    double head_sum = 0.0, acc = 0.0;
-    bool head_closed = false;
+    if (__all_sync(FULL, bits == 0)) {
+      // the whole tile lies in row r0: a plain warp reduction, one emit
+      double acc = 0.0;
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      if (!((vm >> k) & 1u)) continue;
-      if (k > kf && ((bits >> k) & 1u)) {
-        if (j == head_j && !head_closed) {
-          head_sum = acc;
-          head_closed = true;
-        } else {
-          emit(j, acc);
-        }
-        acc = 0.0;
-        ++j;
+      for (int k = 0; k < V; ++k) acc = __dadd_rn(acc, ((vm >> k) & 1u) ? v[k] : 0.0);
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, d));
+      const uint32_t vid = __shfl_sync(FULL, idl, 0);
+      if (lane == 0) {
+        if (!first_start || last_cont) atomicAdd(out + vid, acc);
+        else if (ASSIGN) out[vid] = acc;
+        else out[vid] = __dadd_rn(out[vid], acc);
       }
-      acc = __dadd_rn(acc, v[k]);
-    }
-    // segmented inclusive scan of the lane tails (key = tail row)
-    int key = lane_valid ? (int)j : -1 - lane;
-    double val = acc;
+    } else {
+      s_ids[lane] = idl;
+      // exclusive prefix of row starts over lanes
+      const int cnt = __popc(bits);
+      int incl = cnt;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int k2 = __shfl_up_sync(FULL, key, d);
-      const double v2 = __shfl_up_sync(FULL, val, d);
-      if (lane >= d && k2 == key) val = __dadd_rn(v2, val);
-    }
-    int pk = __shfl_up_sync(FULL, key, 1);
-    const double pv = __shfl_up_sync(FULL, val, 1);
-    if (lane == 0) pk = -1000;
-    int nh = __shfl_down_sync(FULL, lane_valid ? (int)head_j : -1000, 1);
-    if (lane == 31) nh = -1000;
-    if (lane_valid) {
-      if (head_closed) emit(head_j, (pk == (int)head_j) ? __dadd_rn(pv, head_sum) : head_sum);
-      if (nh != (int)j) emit(j, val);
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const uint32_t r_last = r0 + (uint32_t)__shfl_sync(FULL, incl, 31);
+      __syncwarp();
+      const bool lane_valid = vm != 0;
+      const int kf = lane_valid ? __ffs(vm) - 1 : 0;
+      uint32_t j = r0 + (uint32_t)(incl - cnt) + ((bits >> kf) & 1u);
+      const uint32_t sb = bits & ~((2u << kf) - 1u);  // row starts after the lane's first edge
+
+      auto emit = [&](uint32_t row, double x) {
+        const uint32_t rr = row - r0;
+        const uint32_t vid = rr < 32 ? s_ids[rr] : id_map_b[row];
+        if ((row == r0 && !first_start) || (row == r_last && last_cont)) atomicAdd(out + vid, x);
+        else if (ASSIGN) out[vid] = x;
+        else out[vid] = __dadd_rn(out[vid], x);
+      };
+
+      const uint32_t head_j = j;
+      double head_sum = 0.0, acc = 0.0;
+      bool head_closed = false;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if ((sb >> k) & 1u) {
+          if (!head_closed) {
+            head_sum = acc;
+            head_closed = true;
+          } else {
+            emit(j, acc);
+          }
+          acc = 0.0;
+          ++j;
+        }
+        acc = __dadd_rn(acc, ((vm >> k) & 1u) ? v[k] : 0.0);
+      }
+      // segmented inclusive scan of the lane tails (key = tail row)
+      const int key = lane_valid ? (int)j : -1 - lane;
+      double val = acc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int k2 = __shfl_up_sync(FULL, key, d);
+        const double v2 = __shfl_up_sync(FULL, val, d);
+        if (lane >= d && k2 == key) val = __dadd_rn(v2, val);
+      }
+      int pk = __shfl_up_sync(FULL, key, 1);
+      const double pv = __shfl_up_sync(FULL, val, 1);
+      if (lane == 0) pk = -1000;
+      int nh = __shfl_down_sync(FULL, lane_valid ? (int)head_j : -1000, 1);
+      if (lane == 31) nh = -1000;
+      if (lane_valid) {
+        if (head_closed) emit(head_j, (pk == (int)head_j) ? __dadd_rn(pv, head_sum) : head_sum);
+        if (nh != (int)j) emit(j, val);
+      }
+      __syncwarp();
     }
     // rotate the pipeline
 #pragma unroll
@@ -384,7 +408,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
     fw = fwn;
     r0 = r0n;
     idl = idn;
-    __syncwarp();
   }
 }
 
@@ -541,7 +564,7 @@ static void fill_hot(gcb_ctx *ctx, gcb_blocked *bg, const double *vals) {
 // 0.93 / 0.86 / 0.50 per SM cycle with 0 / 128 / 192 KB of shared memory).
 static int prefix_carveout_kb() {
   const char *env = getenv("GCB_CARVE_KB");
-  return env ? atoi(env) : 132;
+  return env ? atoi(env) : 100;
 }
 static int64_t prefix_hot_slots(gcb_ctx *ctx, int nw) {
   int optin = 0;
@@ -553,10 +576,6 @@ static int64_t prefix_hot_slots(gcb_ctx *ctx, int nw) {
   const char *env = getenv("GCB_HOT_K");
   if (env && atoll(env) < K) K = atoll(env);
   return K < 0 ? 0 : K;
-}
-static uint32_t prefix_warm_end(int64_t hot) {
-  const char *env = getenv("GCB_WARM");
-  return env ? (uint32_t)atoll(env) : (uint32_t)(hot + 16384);
 }
 
 static void ensure_prefix_exec(gcb_ctx *ctx, gcb_blocked *bg) {
@@ -600,8 +619,7 @@ static void launch_prefix_nw(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const dou
   if (grid > ctx->num_sms) grid = ctx->num_sms;
   k_pull_prefix<WGT, ASSIGN, NW><<<(unsigned)(grid < 1 ? 1 : grid), NW * 32, smem, ctx->stream>>>(
       bg->col.p, WGT ? bg->w.p : nullptr, bg->rstart.p, bg->id_map.p + rs, bg->tile_row.p + tb, es,
-      ee, bg->h_tile_t0[b], nt, (uint32_t)lo, hot, prefix_warm_end(hot), (uint32_t)Lb,
-      getenv("GCB_L2HINT") ? atoi(getenv("GCB_L2HINT")) : 0, vals, out);
+      ee, bg->h_tile_t0[b], nt, (uint32_t)lo, hot, (uint32_t)Lb, vals, out);
   after_launch(ctx, "k_pull_prefix");
 }
 

@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(512, 2)
 }
 
 static unsigned update_grid(gcb_ctx *ctx, int64_t n) {
-  static int per_sm = getenv("GCB_UPD_CTAS") ? atoi(getenv("GCB_UPD_CTAS")) : 2;
+  static int per_sm = getenv("GCB_UPD_CTAS") ? atoi(getenv("GCB_UPD_CTAS")) : 1 << 20;
   return grid_for((n + 3) / 4, 512, (int64_t)per_sm * ctx->num_sms);
 }
 
