@@ -407,9 +407,8 @@ def run_e2e(args, bg, ctx, stream, flags, steps=None):
                               *(host[k].numpy() for k in ("row_starts", "lro_arena",
                                                           "id_map_arena", "edge_starts",
                                                           "col_arena")))
-        r = gcb.pr_blocked(hb, params, exact=bool(flags & _lib.FLAG_EXACT),
-                           f32_values=bool(flags & _lib.FLAG_F32_VALUES))
-        out.numpy()[...] = r.ranks
+        gcb.pr_blocked(hb, params, exact=bool(flags & _lib.FLAG_EXACT),
+                       f32_values=bool(flags & _lib.FLAG_F32_VALUES), out=out.numpy())
         del hb
 
     step()

@@ -1,27 +1,37 @@
-// gather.cu -- the fast TOCAB pull gather (K2) that accumulates straight into
-// a dense per-vertex vector, optionally with the block's hottest sources
-// staged in shared memory.
+// gather.cu -- the fast TOCAB pull gather (K2): every block's rows are
+// summed straight into a dense per-vertex vector (sums[id_map[row]] += row
+// sum), with the block's hottest sources staged in shared memory.
 //
-// Bottleneck model (ncu, profiles/): a random 8-byte gather through L1TEX
-// costs one wavefront per distinct 128-byte line, ~2 SM cycles each when a
-// warp load touches 32 lines, so the plain gather runs at ~1 edge per 2 cycles
-// per SM (L1/TEX throughput 59-79%, DRAM 13-15%).  Two levers:
-//   * memory-level parallelism: the next tile's tile_row / col_idx / row-end
-//     chunk are prefetched while the current tile's gathers are in flight;
-//   * hot staging: the top-K sources (by out-degree) of each TOCAB block are
-//     copied into shared memory once per launch; R-MAT blocks are
-//     self-similar, so the top ~16-26K sources of a 2^22-wide block carry
-//     ~40-49% of its edges (scale 24), and those edges become LDS.
-// Execution layout (built once, ensure_exec): xcol = col arena with every
-// hot source replaced by 0x80000000 | slot; hot_ids[b][slot] = source id.
-// The reference arena (col) is kept for downloads and the other kernels.
-//
-// Rows that cross a tile boundary are combined with f64 atomics (RED) on the
-// destination's sum; all other rows use a plain read-modify-write (a row's
-// destination appears once per block and blocks are stream-ordered).  The
-// order of the RED contributions is not fixed, so this path is deterministic
-// only up to reassociation of long rows (|err| ~ 1e-16 relative); the exact
+// What bounds it (ncu + microbenchmarks, profiles/ and scripts/mb_*.cu):
+//   * every cold gather is one L1TEX->XBAR request; the SM issues at most ~1
+//     per cycle (l1tex__m_l1tex2xbar_req_cycles_active reaches 94% in a pure
+//     random-gather loop at 0.93 gathers/SM-cycle, scripts/mb_gather.cu);
+//   * a shared-memory hit costs no request (random LDS: ~3.7 per SM-cycle,
+//     scripts/mb_smem.cu), so the hot table is the only way below that floor;
+//   * but misses are staged in L1 lines: the random-LDG rate falls to 0.86 /
+//     0.50 / 0.23 per SM-cycle with 128 / 192 / 220 KB of shared memory, so
+//     the table is sized to a 132 KB carve-out (~16K f64 slots);
+//   * TMA tile::gather4 (0.5/cycle) and DSMEM (0.2-0.6/cycle) are slower.
+// So the kernel is built to issue nothing but the cold gathers on the
+// request path, and as few instructions as possible around them:
+//   * col_idx: one 256-bit load per lane (8 edges = one full sector);
+//   * row boundaries: a 1-bit-per-edge row-start bitmap (one 32-byte sector
+//     per 256-edge tile) -- local rows are never empty (blocking.py:189-201),
+//     so row(q) = tile_row + #row starts in (first, q];
+//   * hot test + LDS/LDG as predicated loads (no divergent branches);
+//   * tiles inside a single row (47% at rmat:24) take a plain warp reduction;
+//     the rest use in-lane runs + a segmented shuffle scan over lane tails;
+//   * ASSIGN: the first block of a pass stores rows (sums is zero) instead of
+//     read-modify-writing them; rows that cross a tile use f64 RED.
+// The order of the RED contributions is not fixed, so this path is
+// deterministic only up to reassociation (|err| ~ 1e-16 relative); the exact
 // mode (pr.cu, k_pull_exact) is the bit-reproducible path.
+//
+// Hot sets: on the degree-ordered copy (relabel.cu) the hot sources of a
+// block are its first `hot` ids, read straight from the value vector; on any
+// other pull graph the top-`hot` sources by out-degree are recoded in an
+// execution copy of the arena (xcol = 0x80000000 | slot) and their values
+// gathered into hotval once per pass (k_fill_hot).
 #include <cstdlib>
 
 #include "gcb_internal.cuh"
@@ -29,220 +39,20 @@
 
 namespace gcb {
 
-#ifndef GCB_GWARPS
-#define GCB_GWARPS 32
-#endif
-constexpr int kGWarps = GCB_GWARPS;  // warps per CTA (1 CTA per SM)
+constexpr int kGWarps = 32;  // warps per CTA (1 CTA per SM)
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kHotBit = 0x80000000u;
-constexpr int kEndsPerWarp = kTileT + 32;
 
-struct TileGeom {
-  int64_t abase, lbase, llo, lhi;
-};
-
-__device__ __forceinline__ TileGeom tile_geom(int64_t t, int64_t t0, int64_t es, int64_t ee) {
-  TileGeom g;
-  g.abase = (t0 + t) * kTileT;
-  g.lbase = g.abase - es;
-  g.llo = g.lbase > 0 ? g.lbase : 0;
-  g.lhi = (g.lbase + kTileT < ee - es) ? g.lbase + kTileT : ee - es;
-  return g;
-}
-
-template <bool WGT, bool HOT>
-__global__ void __launch_bounds__(kGWarps * 32, 1)
-    k_gather(const uint32_t *__restrict__ xcol, const double *__restrict__ w,
-             const uint32_t *__restrict__ lro_b, const uint32_t *__restrict__ id_map_b,
-             const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
-             int64_t ntiles, uint32_t Lb, const double *__restrict__ vals,
-             const double *__restrict__ hotval_b, int hot_k, double *__restrict__ out) {
-  constexpr int V = kTileV;
-  extern __shared__ __align__(16) unsigned char smem[];
-  double *s_hot = reinterpret_cast<double *>(smem);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t *ends = reinterpret_cast<uint32_t *>(smem + (size_t)hot_k * 8) + wid * kEndsPerWarp;
-  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
-  const unsigned FULL = 0xffffffffu;
-  const int64_t stride = (int64_t)gridDim.x * kGWarps;
-
-  if (HOT) {
-    const double2 *src = reinterpret_cast<const double2 *>(hotval_b);
-    double2 *dst = reinterpret_cast<double2 *>(s_hot);
-    for (int i = threadIdx.x; i < hot_k / 2; i += blockDim.x) dst[i] = __ldcg(src + i);
-    __syncthreads();
-  }
-
-  int64_t t = (int64_t)blockIdx.x * kGWarps + wid;
-  if (t < ntiles) {
-  // software pipeline: tile t's row id, col chunk and first row-end chunk
-  uint32_t r0 = tile_row[t];
-  uint4 ca, cb;
-  {
-    const TileGeom g = tile_geom(t, t0, es, ee);
-    const uint4 *cp = reinterpret_cast<const uint4 *>(xcol + g.abase + lane * V);
-    ca = ld_stream_u4(cp, pol_stream);
-    cb = ld_stream_u4(cp + 1, pol_stream);
-  }
-  uint32_t e0 = (r0 + 1 + lane <= Lb) ? lro_b[r0 + 1 + lane] : 0xffffffffu;
-  uint32_t r0_start = lro_b[r0];
-
-  for (; t < ntiles; t += stride) {
-    const TileGeom g = tile_geom(t, t0, es, ee);
-    const int64_t tn = t + stride;
-    const bool has_next = tn < ntiles;
-    uint32_t r0n = 0;
-    uint4 can = make_uint4(0, 0, 0, 0), cbn = make_uint4(0, 0, 0, 0);
-    if (has_next) {
-      r0n = tile_row[tn];
-      const TileGeom gn = tile_geom(tn, t0, es, ee);
-      const uint4 *cp = reinterpret_cast<const uint4 *>(xcol + gn.abase + lane * V);
-      can = ld_stream_u4(cp, pol_stream);
-      cbn = ld_stream_u4(cp + 1, pol_stream);
-    }
-
-    // gathers of the current tile
-    const uint32_t c[V] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-    const int64_t q0 = g.lbase + (int64_t)lane * V;
-    double v[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const int64_t q = q0 + k;
-      double x = 0.0;
-      if (q >= g.llo && q < g.lhi) {
-        if (HOT && (c[k] & kHotBit)) x = s_hot[c[k] & ~kHotBit];
-        else x = ld_keep(vals + c[k], pol_keep);
-      }
-      v[k] = x;
-    }
-    if (WGT) {
-      const double2 *wp = reinterpret_cast<const double2 *>(w + g.abase + lane * V);
-#pragma unroll
-      for (int k2 = 0; k2 < V / 2; ++k2) {
-        const double2 ww = ld_stream_d2(wp + k2, pol_stream);
-        v[2 * k2] = __dmul_rn(ww.x, v[2 * k2]);
-        v[2 * k2 + 1] = __dmul_rn(ww.y, v[2 * k2 + 1]);
-      }
-    }
-    // next tile's row-end chunk + row start (depends on r0n, overlaps the gathers)
-    uint32_t e0n = 0xffffffffu, r0n_start = 0;
-    if (has_next) {
-      e0n = (r0n + 1 + lane <= Lb) ? lro_b[r0n + 1 + lane] : 0xffffffffu;
-      r0n_start = lro_b[r0n];
-    }
-
-    // row-end table of the current tile; j_last = row holding lhi - 1
-    ends[lane] = e0;
-    unsigned below = __ballot_sync(FULL, e0 < (uint32_t)g.lhi);
-    int j_last = __popc(below), nload = 32;
-    while (below == FULL && nload < kTileT) {
-      const uint32_t idx = r0 + 1 + nload + lane;
-      const uint32_t e = idx <= Lb ? lro_b[idx] : 0xffffffffu;
-      ends[nload + lane] = e;
-      below = __ballot_sync(FULL, e < (uint32_t)g.lhi);
-      j_last += __popc(below);
-      nload += 32;
-    }
-    __syncwarp();
-    const bool first_partial = (int64_t)r0_start < g.llo;
-    const bool last_partial = (int64_t)ends[j_last] > g.lhi;
-
-    auto emit = [&](int jj, double x) {
-      const uint32_t vid = id_map_b[r0 + jj];
-      if ((jj == 0 && first_partial) || (jj == j_last && last_partial)) {
-        atomicAdd(out + vid, x);
-      } else {
-        out[vid] = __dadd_rn(out[vid], x);
-      }
-    };
-
-    const int64_t qf = q0 > g.llo ? q0 : g.llo;
-    const bool lane_valid = (qf < g.lhi) && (q0 + V > g.llo);
-    int j = 0;
-    if (lane_valid) {
-      int lo = 0, hi = nload;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if ((int64_t)ends[mid] > qf) hi = mid;
-        else lo = mid + 1;
-      }
-      j = lo;
-    }
-    const int head_j = j;
-    double head_sum = 0.0, acc = 0.0;
-    bool head_closed = false;
-    uint32_t endj = ends[j];
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const int64_t q = q0 + k;
-      if (q < g.llo || q >= g.lhi) continue;
-      if ((uint32_t)q >= endj) {
-        if (j == head_j) {
-          head_sum = acc;
-          head_closed = true;
-        } else {
-          emit(j, acc);
-        }
-        acc = 0.0;
-        ++j;
-        endj = ends[j];
-      }
-      acc = __dadd_rn(acc, v[k]);
-    }
-    int key = lane_valid ? j : -1 - lane;
-    double val = acc;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int k2 = __shfl_up_sync(FULL, key, d);
-      const double v2 = __shfl_up_sync(FULL, val, d);
-      if (lane >= d && k2 == key) val = __dadd_rn(v2, val);
-    }
-    int pk = __shfl_up_sync(FULL, key, 1);
-    const double pv = __shfl_up_sync(FULL, val, 1);
-    if (lane == 0) pk = -1000;
-    int nh = __shfl_down_sync(FULL, lane_valid ? head_j : -1000, 1);
-    if (lane == 31) nh = -1000;
-    if (lane_valid) {
-      if (head_closed) emit(head_j, (pk == head_j) ? __dadd_rn(pv, head_sum) : head_sum);
-      if (nh != j) emit(j, val);
-    }
-    __syncwarp();
-    // rotate the pipeline
-    r0 = r0n;
-    ca = can;
-    cb = cbn;
-    e0 = e0n;
-    r0_start = r0n_start;
-  }
-  }  // t < ntiles
-}
-
-// ---------------------------------------------------------------------------
-// k_pull_prefix: the gather for the degree-ordered layout (relabel.cu).
-//
-// ncu (profiles/r1b_*) put the hot-staged kernel at the L1TEX sector ceiling
-// (~0.9 global sectors per SM cycle; a pure random-gather microbenchmark tops
-// out at 0.95, scripts/mb_gather.cu), so every change here removes sectors or
-// instructions:
-//   * hot table = the block's first H sources (the hottest, by construction)
-//     copied contiguously into shared memory: no recoded arena, no fill pass;
-//   * col_idx streamed with one 256-bit load per lane (8 edges = one full
-//     32-byte sector; the two 128-bit loads it replaces touched 2 sectors);
-//   * row boundaries come from a 1-bit-per-edge row-start bitmap (32 bytes per
-//     256-edge tile, one sector per warp) instead of lro tables + a binary
-//     search in shared memory.  Local rows are never empty (blocking.py:
-//     189-201), so row(q) = tile_row + #row starts in (first, q].
-// Reduction and emission are as in k_gather: in-lane runs, a segmented
-// shuffle scan over lane tails, plain read-modify-write for rows inside the
-// tile and f64 RED for rows that cross a tile boundary.
-// ---------------------------------------------------------------------------
-// One source value: the block's hot prefix from shared memory, everything
-// else from L2 (evict_last keeps the block's value slice resident; no L1
-// allocation, cold lines would only evict each other).  Predicated loads, no
-// branch: the compiler's if/else cost a BSSY/BSYNC pair per edge.
+// One source value: a hot source from shared memory, everything else from
+// L2 (evict_last keeps the block's value slice resident; no L1 allocation --
+// cold lines would only evict each other).  Predicated loads, no branch: the
+// compiler's if/else cost a BSSY/BSYNC pair per edge.
+//   HOTBIT: c is an xcol entry, hot iff bit 31 is set (slot = low bits);
+//   else  : c is a source id, hot iff c - lo < hot (degree-ordered prefix).
+template <bool HOTBIT>
 __device__ __forceinline__ double gather_one(const double *vals, uint32_t c, uint32_t lo,
                                              uint32_t hot, uint32_t s_hot, uint64_t pol) {
-  const uint32_t h = c - lo;
+  const uint32_t h = HOTBIT ? (c ^ kHotBit) : c - lo;
   double x;
   asm("{\n\t.reg .pred p;\n\t"
       "setp.lt.u32 p, %1, %2;\n\t"
@@ -256,13 +66,13 @@ __device__ __forceinline__ double gather_one(const double *vals, uint32_t c, uin
 // ASSIGN: out is all zero before this launch (first block of the pass), so a
 // row that lies inside one tile is stored (out[v] = x) instead of
 // read-modify-written -- no dependent load on the emit path.
-template <bool WGT, bool ASSIGN, int NW>
+template <bool WGT, bool ASSIGN, bool HOTBIT, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
-    k_pull_prefix(const uint32_t *__restrict__ col, const double *__restrict__ w,
-                  const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ id_map_b,
-                  const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
-                  int64_t ntiles, uint32_t lo, int hot, uint32_t Lb,
-                  const double *__restrict__ vals, double *__restrict__ out) {
+    k_pull_hot(const uint32_t *__restrict__ col, const double *__restrict__ w,
+               const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ id_map_b,
+               const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
+               int64_t ntiles, uint32_t lo, int hot, uint32_t Lb, const double *__restrict__ hot_src,
+               const double *__restrict__ vals, double *__restrict__ out) {
   constexpr int V = kTileV;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -274,7 +84,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const unsigned FULL = 0xffffffffu;
   const int64_t stride = (int64_t)gridDim.x * NW;
 
-  for (int i = threadIdx.x; i < hot; i += blockDim.x) s_hot[i] = __ldcg(vals + lo + i);
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) s_hot[i] = __ldcg(hot_src + i);
   __syncthreads();
 
   int64_t t = (int64_t)blockIdx.x * NW + wid;
@@ -302,7 +112,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // gathers first: everything below overlaps their latency
     double v[V];
 #pragma unroll
-    for (int k = 0; k < V; ++k) v[k] = gather_one(vals, c[k], lo, (uint32_t)hot, s_hot_addr, pol_keep);
+    for (int k = 0; k < V; ++k) v[k] = gather_one<HOTBIT>(vals, c[k], lo, (uint32_t)hot, s_hot_addr, pol_keep);
     if (WGT) {
       double ww[V];
       ld_stream_f64x4(w + abase + lane * V, pol_stream, ww);
@@ -462,45 +272,47 @@ __global__ void k_recode(int64_t m, const uint32_t *__restrict__ col,
   }
 }
 
-static size_t ends_bytes() { return (size_t)kGWarps * kEndsPerWarp * sizeof(uint32_t); }
-
-template <bool WGT, bool HOT>
-static void set_smem_attr(size_t bytes) {
-  static size_t done = 0;
-  if (bytes > done) {
-    GCB_CUDA(cudaFuncSetAttribute(k_gather<WGT, HOT>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    done = bytes;
-  }
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+// Shared-memory carve-out (KB; an sm_100 configuration) and the hot slots
+// that fill it; the rest of the 256 KB array is L1 (see the header).
+static int carveout_kb() {
+  const char *env = getenv("GCB_CARVE_KB");
+  return env ? atoi(env) : 132;
 }
-
-// Hot-table size: GCB_HOT_K (slots per block; 0 disables), else what fits in
-// the opt-in shared memory next to the row-end tables.
-static int64_t hot_slots(gcb_ctx *ctx) {
+static int64_t hot_capacity(gcb_ctx *ctx) {
   int optin = 0;
   GCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  int64_t K = ((int64_t)optin - (int64_t)ends_bytes() - 256) / 8;
+  int64_t budget = (int64_t)carveout_kb() * 1024;
+  if (budget > optin + 1024) budget = optin + 1024;
+  // 1 KB per CTA is reserved by the system; the id caches take kGWarps * 128 B
+  int64_t K = (budget - 1024 - (int64_t)kGWarps * 128) / 8;
   const char *env = getenv("GCB_HOT_K");
-  if (env) {
-    const int64_t want = atoll(env);
-    if (want < K) K = want;
-  } else if (K > 8192) {
-    // measured at scale 24 (W = 2^22): 8K slots beat 0 / 16K / 24K -- a larger
-    // carve-out shrinks the L1 that the cold gathers and row tables rely on
-    K = 8192;
-  }
-  return K < 0 ? 0 : (K / 64) * 64;
+  if (env && atoll(env) < K) K = atoll(env);
+  return K < 0 ? 0 : K;
 }
 
+// Row-start bitmap + (non-degree-ordered graphs) hot recode.  Built once.
 void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg) {
   ensure_derived(ctx, bg);
   if (bg->xready) return;
-  int64_t K = hot_slots(ctx);
-  const bool can = bg->direction == 0 && bg->n < (int64_t(1) << 31) && bg->m > 0 && K >= 64;
-  if (can) {
-    const int64_t B = bg->B, n = bg->n;
-    if (bg->width < K) K = ((bg->width + 63) / 64) * 64;  // whole slice fits: every source hot
-    bg->hot_k = K;
+  const int64_t B = bg->B, n = bg->n;
+  const int64_t words = (bg->m + kColPad) / 32 + 16;
+  bg->rstart.alloc(words);
+  GCB_CUDA(cudaMemsetAsync(bg->rstart.p, 0, words * sizeof(uint32_t), ctx->stream));
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+    if (Lb == 0) continue;
+    k_row_start_bits<<<grid_for(Lb + 1, 256, 65536), 256, 0, ctx->stream>>>(
+        Lb, bg->h_edge_starts[b], bg->lro.p + rs + b, bg->rstart.p);
+    after_launch(ctx, "k_row_start_bits");
+  }
+  int64_t K = hot_capacity(ctx);
+  if (K > bg->width) K = bg->width;
+  bg->hot_k = K;
+  if (!bg->is_relabeled && K > 0 && bg->m > 0) {
+    GCB_REQUIRE(n < (int64_t(1) << 31), "hot recode needs vertex ids below 2^31");
     bg->hot_ids.alloc(B * K);
     bg->hotval.alloc(B * K);
     DArray<uint32_t> slot_of(n), k1(bg->width), k2(bg->width), v1(bg->width), v2(bg->width);
@@ -523,151 +335,71 @@ void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg) {
     k_recode<<<grid_for(bg->m, 256, 65536), 256, 0, ctx->stream>>>(bg->m, bg->col.p, slot_of.p,
                                                                    bg->xcol.p);
     after_launch(ctx, "k_recode");
-    sync(ctx);
-  } else {
-    bg->hot_k = 0;
   }
+  sync(ctx);
   bg->xready = true;
 }
 
-template <bool WGT, bool HOT>
-static void launch_gather(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double *vals,
-                          double *out) {
-  const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
-  const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
-  const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
-  const int hot_k = HOT ? (int)bg->hot_k : 0;
-  const size_t smem = (size_t)hot_k * 8 + ends_bytes();
-  set_smem_attr<WGT, HOT>(smem);
-  int64_t grid = ceil_div(nt, kGWarps);
-  if (grid > ctx->num_sms) grid = ctx->num_sms;
-  k_gather<WGT, HOT><<<(unsigned)(grid < 1 ? 1 : grid), kGWarps * 32, smem, ctx->stream>>>(
-      HOT ? bg->xcol.p : bg->col.p, WGT ? bg->w.p : nullptr, bg->lro.p + rs + b, bg->id_map.p + rs,
-      bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt, (uint32_t)Lb, vals,
-      HOT ? bg->hotval.p + b * bg->hot_k : nullptr, hot_k, out);
-  after_launch(ctx, "k_gather");
-}
-
-static void fill_hot(gcb_ctx *ctx, gcb_blocked *bg, const double *vals) {
-  ProfScope ps(ctx, 3);
-  const int64_t cnt = bg->B * bg->hot_k;
-  k_fill_hot<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(cnt, bg->hot_ids.p, vals,
-                                                                 bg->hotval.p);
-  after_launch(ctx, "k_fill_hot");
-}
-
-// ---- degree-ordered layout: row-start bitmap + prefix hot table ----
-// Shared-memory carve-out of the prefix gather (KB; one of the sm_100
-// configurations) and the hot slots that fill it.  The rest of the 256 KB
-// unified array is L1, where the warm tier lives and the cold misses are
-// staged: a larger table starves them (scripts/mb_gather.cu: random LDG at
-// 0.93 / 0.86 / 0.50 per SM cycle with 0 / 128 / 192 KB of shared memory).
-static int prefix_carveout_kb() {
-  const char *env = getenv("GCB_CARVE_KB");
-  return env ? atoi(env) : 100;
-}
-static int64_t prefix_hot_slots(gcb_ctx *ctx, int nw) {
-  int optin = 0;
-  GCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  int64_t budget = (int64_t)prefix_carveout_kb() * 1024;
-  if (budget > optin + 1024) budget = optin + 1024;
-  // 1 KB per CTA is reserved by the system; the id caches take kGWarps * 128 B
-  int64_t K = (budget - 1024 - (int64_t)nw * 128) / 8;
-  const char *env = getenv("GCB_HOT_K");
-  if (env && atoll(env) < K) K = atoll(env);
-  return K < 0 ? 0 : K;
-}
-
-static void ensure_prefix_exec(gcb_ctx *ctx, gcb_blocked *bg) {
-  ensure_derived(ctx, bg);
-  if (bg->rready) return;
-  const int64_t words = (bg->m + kColPad) / 32 + 16;
-  bg->rstart.alloc(words);
-  GCB_CUDA(cudaMemsetAsync(bg->rstart.p, 0, words * sizeof(uint32_t), ctx->stream));
-  for (int64_t b = 0; b < bg->B; ++b) {
-    const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
-    if (Lb == 0) continue;
-    k_row_start_bits<<<grid_for(Lb + 1, 256, 65536), 256, 0, ctx->stream>>>(
-        Lb, bg->h_edge_starts[b], bg->lro.p + rs + b, bg->rstart.p);
-    after_launch(ctx, "k_row_start_bits");
-  }
-  sync(ctx);
-  bg->rready = true;
-}
-
-template <bool WGT, bool ASSIGN, int NW>
-static void launch_prefix_nw(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double *vals,
-                             double *out) {
+template <bool WGT, bool ASSIGN, bool HOTBIT>
+static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double *vals,
+                         double *out) {
   const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
   const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
   const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
   const int64_t lo = b * bg->width, hi = (lo + bg->width < bg->n) ? lo + bg->width : bg->n;
-  const int64_t hot_cap = prefix_hot_slots(ctx, NW);
-  const int hot = (int)(hot_cap < hi - lo ? hot_cap : hi - lo);
-  const size_t smem = (size_t)hot * 8 + NW * 32 * sizeof(uint32_t);
+  const int hot = HOTBIT ? (int)bg->hot_k : (int)(bg->hot_k < hi - lo ? bg->hot_k : hi - lo);
+  const size_t smem = (size_t)hot * 8 + kGWarps * 32 * sizeof(uint32_t);
   static size_t done = 0;
   if (smem > done) {
-    GCB_CUDA(cudaFuncSetAttribute(k_pull_prefix<WGT, ASSIGN, NW>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int pct = (int)(100.0 * prefix_carveout_kb() / 228.0 + 0.99);
-    if (pct > 100) pct = 100;
-    GCB_CUDA(cudaFuncSetAttribute(k_pull_prefix<WGT, ASSIGN, NW>,
-                                  cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    auto kern = k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps>;
+    GCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int pct = (int)(100.0 * carveout_kb() / 228.0 + 0.99);
+    GCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  pct > 100 ? 100 : pct));
     done = smem;
   }
-  int64_t grid = ceil_div(nt, NW);
+  int64_t grid = ceil_div(nt, kGWarps);
   if (grid > ctx->num_sms) grid = ctx->num_sms;
-  k_pull_prefix<WGT, ASSIGN, NW><<<(unsigned)(grid < 1 ? 1 : grid), NW * 32, smem, ctx->stream>>>(
-      bg->col.p, WGT ? bg->w.p : nullptr, bg->rstart.p, bg->id_map.p + rs, bg->tile_row.p + tb, es,
-      ee, bg->h_tile_t0[b], nt, (uint32_t)lo, hot, (uint32_t)Lb, vals, out);
-  after_launch(ctx, "k_pull_prefix");
+  const double *hot_src = HOTBIT ? bg->hotval.p + b * bg->hot_k : vals + lo;
+  k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps>
+      <<<(unsigned)(grid < 1 ? 1 : grid), kGWarps * 32, smem, ctx->stream>>>(
+          HOTBIT ? bg->xcol.p : bg->col.p, WGT ? bg->w.p : nullptr, bg->rstart.p,
+          bg->id_map.p + rs, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt, (uint32_t)lo, hot,
+          (uint32_t)Lb, hot_src, vals, out);
+  after_launch(ctx, "k_pull_hot");
 }
 
-static int prefix_warps() {
-  const char *env = getenv("GCB_PWARPS");
-  return env ? atoi(env) : 32;
-}
-
-template <bool WGT, bool ASSIGN>
-static void launch_prefix(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double *vals, double *out) {
-  switch (prefix_warps()) {
-    case 16: launch_prefix_nw<WGT, ASSIGN, 16>(ctx, bg, b, vals, out); break;
-    case 24: launch_prefix_nw<WGT, ASSIGN, 24>(ctx, bg, b, vals, out); break;
-    default: launch_prefix_nw<WGT, ASSIGN, 32>(ctx, bg, b, vals, out); break;
-  }
+template <bool HOTBIT>
+static void launch_block_any(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, bool wgt, bool assign,
+                             const double *vals, double *out) {
+  if (wgt && assign) launch_block<true, true, HOTBIT>(ctx, bg, b, vals, out);
+  else if (wgt) launch_block<true, false, HOTBIT>(ctx, bg, b, vals, out);
+  else if (assign) launch_block<false, true, HOTBIT>(ctx, bg, b, vals, out);
+  else launch_block<false, false, HOTBIT>(ctx, bg, b, vals, out);
 }
 
 // out[v] += sum over the rows of v in every block (block order); the caller
-// clears out first.
+// clears out first (the first non-empty block stores instead of adding).
 void gather_accum(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights,
                   uint32_t flags, double *out) {
-  if (bg->is_relabeled && getenv("GCB_OLD_PREFIX") == nullptr) {
-    ensure_prefix_exec(ctx, bg);
-    const bool wgt = use_weights && bg->weighted;
-    bool first = true;  // out is zero before the first launch (callers clear it)
-    for (int64_t b = 0; b < bg->B; ++b) {
-      if (bg->h_row_starts[b + 1] == bg->h_row_starts[b]) continue;
-      ProfScope ps(ctx, 0);
-      if (wgt && first) launch_prefix<true, true>(ctx, bg, b, vals, out);
-      else if (wgt) launch_prefix<true, false>(ctx, bg, b, vals, out);
-      else if (first) launch_prefix<false, true>(ctx, bg, b, vals, out);
-      else launch_prefix<false, false>(ctx, bg, b, vals, out);
-      first = false;
-    }
-    return;
-  }
+  (void)flags;
   ensure_exec(ctx, bg);
   const bool wgt = use_weights && bg->weighted;
-  const bool hot = bg->hot_k > 0;
-  if (hot) fill_hot(ctx, bg, vals);
-  (void)flags;
+  const bool hotbit = !bg->is_relabeled && bg->hot_k > 0;
+  if (hotbit) {
+    ProfScope ps(ctx, 3);
+    const int64_t cnt = bg->B * bg->hot_k;
+    k_fill_hot<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(cnt, bg->hot_ids.p, vals,
+                                                                   bg->hotval.p);
+    after_launch(ctx, "k_fill_hot");
+  }
+  bool first = true;
   for (int64_t b = 0; b < bg->B; ++b) {
     if (bg->h_row_starts[b + 1] == bg->h_row_starts[b]) continue;
     ProfScope ps(ctx, 0);
-    if (wgt && hot) launch_gather<true, true>(ctx, bg, b, vals, out);
-    else if (wgt) launch_gather<true, false>(ctx, bg, b, vals, out);
-    else if (hot) launch_gather<false, true>(ctx, bg, b, vals, out);
-    else launch_gather<false, false>(ctx, bg, b, vals, out);
+    if (hotbit) launch_block_any<true>(ctx, bg, b, wgt, first, vals, out);
+    else launch_block_any<false>(ctx, bg, b, wgt, first, vals, out);
+    first = false;
   }
 }
 

@@ -46,8 +46,18 @@ int set_last_error(int code, const char *msg);
   }
 
 // ---------------------------------------------------------------------------
-// device memory: RAII owner (cudaFree on destruction).
+// device memory: RAII owner over the device's default stream-ordered pool.
+// Graph uploads allocate and free several GB per call; cudaMalloc/cudaFree
+// of fresh address ranges cost 5-100 ms per upload at scale 24
+// (scripts/e2e_phases.py), the pool (release threshold raised in
+// gcb_ctx_create) reuses them.  Semantics stay those of cudaMalloc/cudaFree:
+// the allocation is complete before it is handed out, and a release waits for
+// the device (cudaFree's implicit synchronisation), so buffers may be used on
+// any stream.
 // ---------------------------------------------------------------------------
+void *device_alloc(size_t bytes);   // ctx.cu
+void device_free(void *p);          // ctx.cu
+
 template <typename T>
 struct DArray {
   T *p = nullptr;
@@ -66,19 +76,13 @@ struct DArray {
     release();
     n = count;
     size_t bytes = (count ? count : 1) * sizeof(T);
-    cudaError_t e = cudaMalloc((void **)&p, bytes);
-    if (e != cudaSuccess) {
-      p = nullptr;
-      n = 0;
-      (void)cudaGetLastError();
-      fail(GCB_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
-    }
+    p = static_cast<T *>(device_alloc(bytes));
   }
   void ensure(size_t count) {
     if (n < count || p == nullptr) alloc(count);
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) device_free(p);
     p = nullptr;
     n = 0;
   }
@@ -157,14 +161,13 @@ struct gcb_blocked {
   int64_t R = 0;                     // merge ranges (ceil(n / kMergeK))
   gcb::DArray<int64_t> bounds;       // [B][R+1] arena positions per range
 
-  // ---- execution layout of the fast accumulate gather (ensure_exec) ----
+  // ---- execution layout of the fast accumulate gather (gather.cu ensure_exec) ----
   bool xready = false;
   int64_t hot_k = 0;                 // hot slots per block (0: staging disabled)
   gcb::DArray<uint32_t> xcol;        // col arena recoded: 0x80000000|slot for hot sources
+                                     // (graphs that are not degree-ordered)
   gcb::DArray<uint32_t> hot_ids;     // [B][hot_k] source id of each slot (or ~0u)
   gcb::DArray<double> hotval;        // [B][hot_k] staged values for the next gather
-  // degree-ordered copies (is_relabeled): row-start bitmap of the arena
-  bool rready = false;
   gcb::DArray<uint32_t> rstart;      // bit q: arena edge q starts a local row
 
   // ---- workspaces (grown on demand) ----
@@ -178,6 +181,7 @@ struct gcb_blocked {
 
   // ---- degree-ordered execution copy of a pull graph (relabel.cu) ----
   bool is_relabeled = false;         // this object is such a copy
+  int64_t fast_iters = 0;            // fast-mode passes run on this graph (tiering)
   gcb_blocked *rl = nullptr;         // the copy (owned), built on first fast call
   gcb::DArray<uint32_t> rl_perm;     // [n] original id -> renumbered id
 
@@ -280,7 +284,7 @@ void cub_sort_pairs_desc_u32_u32(gcb_ctx *ctx, uint32_t *keys, uint32_t *keys_al
 void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sums,
                   bool use_weights, uint32_t flags, int64_t block_only);
 // relabel.cu: degree-ordered execution copy of a pull graph
-bool relabel_enabled(const gcb_blocked *bg, uint32_t flags);
+bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters);
 gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg);
 void permute_in(gcb_ctx *ctx, const gcb_blocked *bg, const double *x, double *x_new);
 void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, double *y);

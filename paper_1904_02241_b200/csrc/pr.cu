@@ -674,7 +674,7 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   const int64_t n = bg->n;
   const bool exact = flags & GCB_FLAG_EXACT;
   const bool push = bg->direction == 1;
-  if (!(flags & GCB_FLAG_F32_VALUES) && !deg_override && relabel_enabled(bg, flags)) {
+  if (!(flags & GCB_FLAG_F32_VALUES) && !deg_override && relabel_enabled(bg, flags, max_iters)) {
     // run on the degree-ordered copy (relabel.cu); ranks come back in input order
     gcb_blocked *rl = ensure_relabeled(ctx, bg);
     rl->ranks.ensure(n);
@@ -879,7 +879,7 @@ int gcb_accumulate_ranges(gcb_ctx *ctx, gcb_blocked *bg, const double *partials_
 // y = pull gather of x over a blocking, accumulated block by block
 static void pull_spmv(gcb_ctx *ctx, gcb_blocked *bg, const double *x, bool weights, uint32_t flags,
                       double *y) {
-  if (bg->n > 0 && relabel_enabled(bg, flags)) {
+  if (bg->n > 0 && relabel_enabled(bg, flags, 1)) {
     gcb_blocked *rl = ensure_relabeled(ctx, bg);
     rl->contrib.ensure(bg->n);
     rl->sums.ensure(bg->n);

@@ -205,13 +205,25 @@ def pr_baseline(g: CsrGraph, direction: str, params: PrParams = PrParams(),
     return PrResult(ranks, iters, conv)
 
 
+def _out_buffer(out, n: int) -> np.ndarray:
+    """Caller-provided result buffer (e.g. pinned host memory, so the ranks
+    come back by DMA) or a fresh array."""
+    if out is None:
+        return np.empty(n, dtype=np.float64)
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == (n,)
+            and out.flags.c_contiguous and out.flags.writeable):
+        raise ValueError(f"out must be a writeable contiguous float64 array of length {n}")
+    return out
+
+
 def pr_blocked(bg: BlockedGraph, params: PrParams = PrParams(), k: int = DEFAULT_RANGE_WIDTH,
                threads: int = 1, *, exact: bool = False, f32_values: bool = False,
-               l2_window: bool = True) -> PrResult:
+               l2_window: bool = True, out=None) -> PrResult:
     """PageRank over a TOCAB blocking (kernels.py:367-405) on the B200.
 
     ``k`` (merge range width) is validated; results are k-invariant bitwise.
-    ``f32_values`` gathers an f32 copy of the contributions (sums stay f64)."""
+    ``f32_values`` gathers an f32 copy of the contributions (sums stay f64).
+    ``out`` (extension): float64[n] the ranks are written into and returned."""
     if bg.scheme != "tocab":
         raise NotImplementedError("the cb ablation scheme is not implemented on the device")
     if int(k) < 1:
@@ -219,7 +231,7 @@ def pr_blocked(bg: BlockedGraph, params: PrParams = PrParams(), k: int = DEFAULT
     n = bg.num_vertices
     (1.0 - params.damping) / n  # ZeroDivisionError on n == 0 (kernels.py:377)
     h = bg.device()
-    ranks = np.empty(n, dtype=np.float64)
+    ranks = _out_buffer(out, n)
     iters, conv = _pr_call(h.ctx._lib.gcb_pr_blocked, h.ctx.handle, h.raw, params.damping,
                            params.tol, params.max_iters, int(k),
                            _flags(exact, f32_values, l2_window), _lib.ptr(ranks, _lib.P_dbl))
@@ -350,14 +362,15 @@ def spmv(g: CsrGraph, x, direction: str = "pull", *, exact: bool = False) -> np.
 
 
 def spmv_blocked(bg: BlockedGraph, x, k: int = DEFAULT_RANGE_WIDTH, threads: int = 1, *,
-                 exact: bool = False) -> np.ndarray:
-    """Blocked y = A x over a TOCAB blocking (kernels.py:431-487)."""
+                 exact: bool = False, out=None) -> np.ndarray:
+    """Blocked y = A x over a TOCAB blocking (kernels.py:431-487).  ``out``
+    (extension): float64[n] y is written into and returned."""
     if bg.scheme != "tocab":
         raise NotImplementedError("the cb ablation scheme is not implemented on the device")
     xv = _f64(x, bg.num_vertices)
     if int(k) < 1:
         raise ValueError("range width k must be >= 1")
-    y = np.empty(bg.num_vertices, dtype=np.float64)
+    y = _out_buffer(out, bg.num_vertices)
     h = bg.device()
     _lib.check(h.ctx._lib.gcb_spmv_blocked(h.ctx.handle, h.raw, _lib.ptr(xv, _lib.P_dbl), int(k),
                                            _flags(exact), _lib.ptr(y, _lib.P_dbl)),
