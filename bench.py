@@ -321,29 +321,39 @@ def run_ours(args):
     peak *= world  # aggregate HBM of the job
     b_alg = algorithmic_bytes_pr(n, m)
     achieved = b_alg / t_iter_s / 1e9
-    # gather kernel alone: its share of the algorithmic bytes = col + contributions read
+    # dominant kernel (the pull gather, k_pull_hot): SURVEY 8(d) per-edge and
+    # per-vertex bytes it must move -- col_idx 4 B/edge, the contribution read
+    # 8 B/vertex, the row pointer 4 B/vertex -- over the launches of one iteration
     b_gather = 4 * m + 8 * n + 4 * (n + 1)
-    roofline = {
-        "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_kind,
-        "scope": "one PageRank iteration (all launches); B_alg = 4|E| + 4(|V|+1) + 36|V| "
-                 f"= {b_alg} bytes",
-        "kernels_ms_per_iter": {k: round(v, 4) for k, v in per_iter.items()},
-        "gather_kernel": {
-            "launches_per_iter": gather_groups,
-            "ms_per_iter": round(gather_ms, 4),
-            "algorithmic_bytes": b_gather,
-            "achieved_gbs": round(b_gather / (gather_ms / 1e3) / 1e9, 1) if gather_ms else None,
-            "share_of_iteration": round(gather_ms / (t_iter_s * 1e3), 3),
-        },
-    }
+    gather_s = gather_ms / 1e3
+    g_achieved = b_gather / gather_s / 1e9 if gather_ms else None
+    traffic = None
     prof_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof_file):
         try:
             with open(prof_file) as fh:
-                roofline["traffic"] = json.load(fh).get("traffic_per_iteration")
+                traffic = json.load(fh).get("k_pull_hot_bytes_per_iteration")
         except Exception:
-            pass
+            traffic = None
+    roofline = {
+        "bound": "hbm", "kernel": "k_pull_hot (TOCAB pull gather, gather.cu)",
+        "achieved": round(g_achieved, 1) if g_achieved else None, "peak": peak, "unit": "GB/s",
+        "frac": round(g_achieved / peak, 4) if g_achieved else None,
+        "traffic": traffic, "peak_source": peak_kind,
+        "algorithmic_bytes_per_iteration": b_gather,
+        "launches_per_iteration": gather_groups,
+        "ms_per_iteration": round(gather_ms, 4),
+        "share_of_iteration": round(gather_ms / (t_iter_s * 1e3), 3),
+        "scope": "per iteration (all gather launches); traffic = ncu dram bytes of the same "
+                 "launches (profiles/ncu_traffic.json)",
+        "iteration": {
+            "achieved": round(achieved, 1), "frac": round(achieved / peak, 4),
+            "algorithmic_bytes": b_alg,
+            "scope": "one whole PageRank iteration (every launch); B_alg = 4|E| + 4(|V|+1) + "
+                     "36|V| (SURVEY 8d) -- the metric's 'fraction of HBM roofline'",
+        },
+        "kernels_ms_per_iter": {k: round(v, 4) for k, v in per_iter.items()},
+    }
 
     # ---- e2e: public host-buffer API, arenas from pinned memory each step ----
     e2e = None

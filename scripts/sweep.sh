@@ -8,6 +8,6 @@ for cfg in "$@"; do
     python -c "import sys,json
 l=sys.stdin.read()
 try:
-  d=json.loads(l); r=d['roofline']; print(d['value'], d['ms_per_step'], r['frac'], r['kernels_ms_per_iter'], d['setup_s'])
+  d=json.loads(l); r=d['roofline']; print(d['value'], d['ms_per_step'], r['iteration']['frac'], r['kernels_ms_per_iter'], d['setup_s'])
 except Exception: print('FAIL', l[-600:])" >> "$out"
 done
