@@ -36,6 +36,7 @@
 
 #include "gcb_internal.cuh"
 #include "ldst.cuh"
+#include "tiles.cuh"
 
 namespace gcb {
 
@@ -120,98 +121,26 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
       for (int k = 0; k < V; ++k) v[k] = __dmul_rn(ww[k], v[k]);
     }
-    // valid tile positions [llo, lhi); lane's valid k in [a, z)
+    // valid tile positions [llo, lhi); row-start bits of the lane's edges
     const int llo = es > abase ? (int)(es - abase) : 0;
     const int lhi = ee - abase < kTileT ? (int)(ee - abase) : kTileT;
-    const int a = llo - lane * V, z = lhi - lane * V;
-    const uint32_t vm = (z <= 0 || a >= V) ? 0u
-                        : ((0xffu >> (V - (z < V ? z : V))) & (0xffu << (a > 0 ? a : 0)));
-    // row-start bits of the lane's edges (valid ones; the tile's first valid
-    // edge dropped -- its row is r0)
-    const uint32_t wl = __shfl_sync(FULL, fw, lane >> 2);
-    uint32_t bits = (wl >> ((lane & 3) * 8)) & vm;
-    if (a >= 0 && a < V) bits &= ~(1u << a);
-    const bool first_start = (__shfl_sync(FULL, fw, llo >> 5) >> (llo & 31)) & 1u;
-    const bool last_cont = (lhi == kTileT) && !(__shfl_sync(FULL, fw, 8) & 1u);
+    const TileBits tbits = tile_bits(fw, llo, lhi, lane);
     // next tile's id cache (its first row is known by now)
     uint32_t idn = 0;
     if (has_next && r0n + lane < Lb) idn = id_map_b[r0n + lane];
-
-    if (__all_sync(FULL, bits == 0)) {
-      // the whole tile lies in row r0: a plain warp reduction, one emit
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < V; ++k) acc = __dadd_rn(acc, ((vm >> k) & 1u) ? v[k] : 0.0);
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, d));
-      const uint32_t vid = __shfl_sync(FULL, idl, 0);
-      if (lane == 0) {
-        if (!first_start || last_cont) atomicAdd(out + vid, acc);
-        else if (ASSIGN) out[vid] = acc;
-        else out[vid] = __dadd_rn(out[vid], acc);
-      }
-    } else {
-      s_ids[lane] = idl;
-      // exclusive prefix of row starts over lanes
-      const int cnt = __popc(bits);
-      int incl = cnt;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(FULL, incl, d);
-        if (lane >= d) incl += y;
-      }
-      const uint32_t r_last = r0 + (uint32_t)__shfl_sync(FULL, incl, 31);
-      __syncwarp();
-      const bool lane_valid = vm != 0;
-      const int kf = lane_valid ? __ffs(vm) - 1 : 0;
-      uint32_t j = r0 + (uint32_t)(incl - cnt) + ((bits >> kf) & 1u);
-      const uint32_t sb = bits & ~((2u << kf) - 1u);  // row starts after the lane's first edge
-
-      auto emit = [&](uint32_t row, double x) {
-        const uint32_t rr = row - r0;
-        const uint32_t vid = rr < 32 ? s_ids[rr] : id_map_b[row];
-        if ((row == r0 && !first_start) || (row == r_last && last_cont)) atomicAdd(out + vid, x);
-        else if (ASSIGN) out[vid] = x;
-        else out[vid] = __dadd_rn(out[vid], x);
-      };
-
-      const uint32_t head_j = j;
-      double head_sum = 0.0, acc = 0.0;
-      bool head_closed = false;
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        if ((sb >> k) & 1u) {
-          if (!head_closed) {
-            head_sum = acc;
-            head_closed = true;
-          } else {
-            emit(j, acc);
-          }
-          acc = 0.0;
-          ++j;
-        }
-        acc = __dadd_rn(acc, ((vm >> k) & 1u) ? v[k] : 0.0);
-      }
-      // segmented inclusive scan of the lane tails (key = tail row)
-      const int key = lane_valid ? (int)j : -1 - lane;
-      double val = acc;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int k2 = __shfl_up_sync(FULL, key, d);
-        const double v2 = __shfl_up_sync(FULL, val, d);
-        if (lane >= d && k2 == key) val = __dadd_rn(v2, val);
-      }
-      int pk = __shfl_up_sync(FULL, key, 1);
-      const double pv = __shfl_up_sync(FULL, val, 1);
-      if (lane == 0) pk = -1000;
-      int nh = __shfl_down_sync(FULL, lane_valid ? (int)head_j : -1000, 1);
-      if (lane == 31) nh = -1000;
-      if (lane_valid) {
-        if (head_closed) emit(head_j, (pk == (int)head_j) ? __dadd_rn(pv, head_sum) : head_sum);
-        if (nh != (int)j) emit(j, val);
-      }
-      __syncwarp();
-    }
+    s_ids[lane] = idl;
+    __syncwarp();
+    tile_reduce<double>(
+        v, tbits, r0, lane, 0.0, [](double x, double y) { return __dadd_rn(x, y); },
+        [&](uint32_t row, double x, uint32_t r_last) {
+          const uint32_t rr = row - r0;
+          const uint32_t vid = rr < 32 ? s_ids[rr] : id_map_b[row];
+          if ((row == r0 && !tbits.first_start) || (row == r_last && tbits.last_cont))
+            atomicAdd(out + vid, x);
+          else if (ASSIGN) out[vid] = x;
+          else out[vid] = __dadd_rn(out[vid], x);
+        });
+    __syncwarp();
     // rotate the pipeline
 #pragma unroll
     for (int k = 0; k < V; ++k) c[k] = cn[k];
@@ -293,21 +222,28 @@ static int64_t hot_capacity(gcb_ctx *ctx) {
   return K < 0 ? 0 : K;
 }
 
-// Row-start bitmap + (non-degree-ordered graphs) hot recode.  Built once.
-void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg) {
+// Row-start bitmap of the arena (tiles.cuh).  Built once.
+void ensure_row_bits(gcb_ctx *ctx, gcb_blocked *bg) {
   ensure_derived(ctx, bg);
-  if (bg->xready) return;
-  const int64_t B = bg->B, n = bg->n;
+  if (bg->rstart.p) return;
   const int64_t words = (bg->m + kColPad) / 32 + 16;
   bg->rstart.alloc(words);
   GCB_CUDA(cudaMemsetAsync(bg->rstart.p, 0, words * sizeof(uint32_t), ctx->stream));
-  for (int64_t b = 0; b < B; ++b) {
+  for (int64_t b = 0; b < bg->B; ++b) {
     const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
     if (Lb == 0) continue;
     k_row_start_bits<<<grid_for(Lb + 1, 256, 65536), 256, 0, ctx->stream>>>(
         Lb, bg->h_edge_starts[b], bg->lro.p + rs + b, bg->rstart.p);
     after_launch(ctx, "k_row_start_bits");
   }
+}
+
+// Row-start bitmap + (non-degree-ordered graphs) hot recode.  Built once.
+void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg) {
+  ensure_derived(ctx, bg);
+  if (bg->xready) return;
+  const int64_t B = bg->B, n = bg->n;
+  ensure_row_bits(ctx, bg);
   int64_t K = hot_capacity(ctx);
   if (K > bg->width) K = bg->width;
   bg->hot_k = K;

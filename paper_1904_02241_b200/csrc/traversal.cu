@@ -11,6 +11,7 @@
 #include <climits>
 
 #include "gcb_internal.cuh"
+#include "tiles.cuh"
 
 namespace gcb {
 
@@ -256,31 +257,52 @@ __global__ void k_sssp_push(int64_t qsize, const uint32_t *__restrict__ queue,
   }
 }
 
-__global__ void k_sssp_pull_block(int64_t Lb, const uint32_t *__restrict__ lro_b,
-                                  const uint32_t *__restrict__ id_map_b,
-                                  const uint32_t *__restrict__ col_b, const double *__restrict__ w_b,
-                                  const uint32_t *__restrict__ front_bits,
-                                  long long *__restrict__ dist, uint8_t *__restrict__ next) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Lb;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = id_map_b[i];
-    long long best = dist[v];
-    const long long before = best;
-    const uint32_t e1 = lro_b[i + 1];
-    for (uint32_t e = lro_b[i]; e < e1; ++e) {
-      const uint32_t u = col_b[e];
-      if (front_bits[u >> 5] >> (u & 31) & 1u) {
-        const long long du = dist[u];
-        if (du != LLONG_MAX) {
-          const long long cand = du + (long long)w_b[e];
-          if (cand < best) best = cand;
+// Edge-balanced form of the pull round (the thread-per-row kernel above left
+// a hub row of ~370K in-edges to one thread: 679 ms for SSSP at rmat:24).
+// Warp per 256-edge tile; candidate dist[u] + w for frontier sources u;
+// per-row min via tiles.cuh; every row piece lands with a 64-bit atomicMin
+// (idempotent, so pieces of rows that cross tiles need no special case).
+__global__ void __launch_bounds__(256)
+    k_sssp_pull_tiles(const uint32_t *__restrict__ col, const double *__restrict__ w,
+                      const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ id_map_b,
+                      const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
+                      int64_t ntiles, const uint32_t *__restrict__ front_bits,
+                      long long *__restrict__ dist, uint8_t *__restrict__ next) {
+  constexpr int V = kTileV;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nw) {
+    const int64_t abase = (t0 + t) * kTileT;
+    const uint4 *cp = reinterpret_cast<const uint4 *>(col + abase + lane * V);
+    const uint4 ca = __ldcs(cp), cb = __ldcs(cp + 1);
+    const uint32_t c[V] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+    const uint32_t fw = rstart[(abase >> 5) + (lane < 8 ? lane : 8)];
+    const uint32_t r0 = tile_row[t];
+    const int llo = es > abase ? (int)(es - abase) : 0;
+    const int lhi = ee - abase < kTileT ? (int)(ee - abase) : kTileT;
+    const TileBits tb = tile_bits(fw, llo, lhi, lane);
+    long long cand[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      cand[k] = LLONG_MAX;
+      if ((tb.vm >> k) & 1u) {
+        const uint32_t u = c[k];
+        if ((front_bits[u >> 5] >> (u & 31)) & 1u) {
+          const long long du = dist[u];
+          if (du != LLONG_MAX) cand[k] = du + (long long)w[abase + lane * V + k];
         }
       }
     }
-    if (best < before) {
-      const long long old = atomicMin(&dist[v], best);
-      if (best < old) next[v] = 1;
-    }
+    tile_reduce<long long>(
+        cand, tb, r0, lane, LLONG_MAX, [](long long a, long long b) { return a < b ? a : b; },
+        [&](uint32_t row, long long x, uint32_t) {
+          if (x == LLONG_MAX) return;
+          const uint32_t v = id_map_b[row];
+          if (x < dist[v]) {
+            const long long old = atomicMin(&dist[v], x);
+            if (x < old) next[v] = 1;
+          }
+        });
   }
 }
 
@@ -436,7 +458,7 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
   if (bg) {
     GCB_REQUIRE(bg->n == g->n && bg->direction == 0 && bg->weighted,
                 "g_blocked must be a weighted pull blocking of g");
-    ensure_derived(ctx, bg);
+    ensure_row_bits(ctx, bg);
   }
   const int64_t n = g->n;
   DArray<int64_t> dist(n ? n : 1);
@@ -476,11 +498,13 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
       for (int64_t b = 0; b < bg->B; ++b) {
         const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
         if (!Lb) continue;
-        const int64_t es = bg->h_edge_starts[b];
-        k_sssp_pull_block<<<grid_for(Lb, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-            Lb, bg->lro.p + rs + b, bg->id_map.p + rs, bg->col.p + es, bg->w.p + es, F.bits.p,
-            (long long *)dist.p, F.next.p);
-        after_launch(ctx, "k_sssp_pull_block");
+        const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
+        k_sssp_pull_tiles<<<grid_for(nt * 32, 256, (int64_t)ctx->num_sms * 8), 256, 0,
+                            ctx->stream>>>(bg->col.p, bg->w.p, bg->rstart.p, bg->id_map.p + rs,
+                                           bg->tile_row.p + tb, bg->h_edge_starts[b],
+                                           bg->h_edge_starts[b + 1], bg->h_tile_t0[b], nt,
+                                           F.bits.p, (long long *)dist.p, F.next.p);
+        after_launch(ctx, "k_sssp_pull_tiles");
       }
     }
     // compact next flags into the queue
