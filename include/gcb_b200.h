@@ -228,6 +228,20 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
              uint8_t *directions_host, int64_t max_rounds, int64_t *rounds);
 /* Weakly connected components, labels = min vertex id. */
 int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_components);
+/* Betweenness centrality (bc traversal.py:257-278): for each source in order,
+ * a forward sweep with path counts (push / blocked-pull per choose_direction,
+ * bg_pull NULL = partition_tocab(transpose(g), "pull", max(1, n // 8))) and
+ * the dependency pass (bc_backward traversal.py:212-236); centrality[n] =
+ * sum of the per-source dependencies (ordered pairs, endpoints excluded).
+ * flags: GCB_FLAG_EXACT sums every vertex's out-edges in CSR order
+ * (bit-identical to the reference); default = warp reductions. */
+int gcb_bc(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, const int64_t *sources_host,
+           int64_t num_sources, int mode, int64_t capacity_bytes, int64_t value_bytes,
+           uint32_t flags, double *centrality_host);
+/* bc_backward traversal.py:212-236 for a given forward state: depth[n]
+ * (INT32_MAX = unreached), sigma[n]; writes delta[n] with delta[source] = 0. */
+int gcb_bc_backward(gcb_ctx *ctx, const gcb_csr *g, const int32_t *depth_host,
+                    const double *sigma_host, int64_t source, uint32_t flags, double *delta_host);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

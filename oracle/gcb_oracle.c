@@ -616,3 +616,96 @@ int orc_cc(int64_t n, const int64_t *ro, const uint32_t *col, uint32_t *label) {
   for (int64_t v = 0; v < n; ++v) label[v] = uf_find(label, (uint32_t)v);
   return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * Betweenness centrality (traversal.py:212-278).
+ * Forward sweep with path counts (forward_push_step traversal.py:121-140 with
+ * accumulate_sigma): level queues ascending (np.unique), sigma of a newly
+ * reached vertex = 0.0 + sum of its frontier in-neighbours' sigma in the
+ * np.bincount order (queue order, then CSR order).  Direction-invariant for
+ * integer-valued sigma (test_traversal.py:221-233), so the oracle pushes.
+ * ------------------------------------------------------------------------- */
+static int cmp_u32(const void *a, const void *b) {
+  uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+  return x < y ? -1 : x > y;
+}
+
+int orc_bfs_sigma(int64_t n, const int64_t *ro, const uint32_t *col, int64_t source,
+                  int32_t *depth, double *sigma) {
+  if (source < 0 || source >= n) return 1;
+  uint32_t *q = (uint32_t *)malloc((size_t)(n + 1) * sizeof(uint32_t));
+  double *add = (double *)calloc((size_t)(n ? n : 1), sizeof(double));
+  if (!q || !add) { free(q); free(add); return 2; }
+  for (int64_t v = 0; v < n; ++v) { depth[v] = INT32_MAX; sigma[v] = 0.0; }
+  depth[source] = 0;
+  sigma[source] = 1.0;
+  int64_t head = 0, tail = 0;
+  q[tail++] = (uint32_t)source;
+  int32_t level = 0;
+  while (head < tail) {
+    int64_t lo = head, hi = tail;
+    /* stamp the next level (unvisited destinations), queue them */
+    for (int64_t i = lo; i < hi; ++i)
+      for (int64_t e = ro[q[i]]; e < ro[q[i] + 1]; ++e) {
+        uint32_t v = col[e];
+        if (depth[v] == INT32_MAX) { depth[v] = level + 1; q[tail++] = v; }
+      }
+    qsort(q + hi, (size_t)(tail - hi), sizeof(uint32_t), cmp_u32);
+    /* bincount(dsts[takes], weights=sigma[srcs[takes]]) in queue x CSR order */
+    for (int64_t i = lo; i < hi; ++i)
+      for (int64_t e = ro[q[i]]; e < ro[q[i] + 1]; ++e) {
+        uint32_t v = col[e];
+        if (depth[v] == level + 1) add[v] += sigma[q[i]];
+      }
+    for (int64_t i = hi; i < tail; ++i) { sigma[q[i]] += add[q[i]]; add[q[i]] = 0.0; }
+    head = hi;
+    ++level;
+  }
+  free(q);
+  free(add);
+  return 0;
+}
+
+/* bc_backward traversal.py:212-236: deepest level first, per vertex the
+ * qualifying out-edges summed from 0.0 in CSR order, then delta += that. */
+int orc_bc_backward(int64_t n, const int64_t *ro, const uint32_t *col, const int32_t *depth,
+                    const double *sigma, int64_t source, double *delta) {
+  int32_t maxd = -1;
+  for (int64_t v = 0; v < n; ++v) {
+    delta[v] = 0.0;
+    if (depth[v] != INT32_MAX && depth[v] > maxd) maxd = depth[v];
+  }
+  for (int32_t level = maxd - 1; level >= 0; --level)
+    for (int64_t v = 0; v < n; ++v) {
+      if (depth[v] != level) continue;
+      double acc = 0.0;
+      for (int64_t e = ro[v]; e < ro[v + 1]; ++e) {
+        uint32_t w = col[e];
+        if (depth[w] == level + 1) acc += (sigma[v] / sigma[w]) * (1.0 + delta[w]);
+      }
+      delta[v] += acc;
+    }
+  if (source >= 0 && source < n) delta[source] = 0.0;
+  return 0;
+}
+
+/* bc traversal.py:257-278: centrality += delta per source, in order. */
+int orc_bc(int64_t n, const int64_t *ro, const uint32_t *col, const int64_t *sources,
+           int64_t num_sources, double *centrality) {
+  int32_t *depth = (int32_t *)malloc((size_t)(n ? n : 1) * sizeof(int32_t));
+  double *sigma = (double *)malloc((size_t)(n ? n : 1) * sizeof(double));
+  double *delta = (double *)malloc((size_t)(n ? n : 1) * sizeof(double));
+  if (!depth || !sigma || !delta) { free(depth); free(sigma); free(delta); return 2; }
+  for (int64_t v = 0; v < n; ++v) centrality[v] = 0.0;
+  int rc = 0;
+  for (int64_t i = 0; i < num_sources && !rc; ++i) {
+    rc = orc_bfs_sigma(n, ro, col, sources[i], depth, sigma);
+    if (!rc) rc = orc_bc_backward(n, ro, col, depth, sigma, sources[i], delta);
+    if (!rc)
+      for (int64_t v = 0; v < n; ++v) centrality[v] += delta[v];
+  }
+  free(depth);
+  free(sigma);
+  free(delta);
+  return rc;
+}

@@ -52,10 +52,14 @@ from .kernels import (
 from .traversal import (
     INF_DEPTH,
     INF_DIST,
+    BcResult,
     BfsResult,
     DirectionPolicy,
     SsspResult,
     TraversalState,
+    bc,
+    bc_backward,
+    bc_single_source,
     bfs,
     choose_direction,
     forward_pull_step,

@@ -705,3 +705,366 @@ extern "C" int gcb_bfs_step(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull
   sync(ctx);
   GCB_API_END
 }
+
+// ---------------------------------------------------------------------------
+// Betweenness centrality (bc / bc_single_source / bc_backward,
+// traversal.py:212-278): a forward sweep with path counts (the BFS steps
+// above, push or blocked pull per choose_direction) then the dependency pass
+// deepest level first:
+//   delta[v] = sum over out-edges v->w with depth[w] == depth[v] + 1 of
+//              (sigma[v] / sigma[w]) * (1 + delta[w])        (traversal.py:224-234)
+// delta[source] = 0; centrality accumulates delta over the sources in order.
+// Exact mode sums each vertex's out-edges sequentially in CSR order (the
+// np.bincount order of traversal.py:233) -> bit-identical; fast mode reduces
+// each vertex's edges across a warp (|err| ~ 1e-16 relative).
+// ---------------------------------------------------------------------------
+namespace gcb {
+
+__device__ __forceinline__ double bc_term(double sv, double sw, double dw) {
+  return __dmul_rn(__ddiv_rn(sv, sw), __dadd_rn(1.0, dw));
+}
+
+// thread per vertex of the level, sequential in CSR order (exact)
+__global__ void k_bc_back_exact(int64_t cnt, const uint32_t *__restrict__ verts, int32_t level,
+                                const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
+                                const int32_t *__restrict__ depth, const double *__restrict__ sigma,
+                                double *__restrict__ delta) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = verts[i];
+    const double sv = sigma[v];
+    double acc = 0.0;
+    for (int64_t e = ro[v]; e < ro[v + 1]; ++e) {
+      const uint32_t w = col[e];
+      if (depth[w] == level + 1) acc = __dadd_rn(acc, bc_term(sv, sigma[w], delta[w]));
+    }
+    delta[v] = __dadd_rn(delta[v], acc);
+  }
+}
+
+// warp per vertex of the level (fast)
+__global__ void k_bc_back_warp(int64_t cnt, const uint32_t *__restrict__ verts, int32_t level,
+                               const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
+                               const int32_t *__restrict__ depth, const double *__restrict__ sigma,
+                               double *__restrict__ delta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < cnt; i += nw) {
+    const uint32_t v = verts[i];
+    const double sv = sigma[v];
+    double acc = 0.0;
+    for (int64_t e = ro[v] + lane; e < ro[v + 1]; e += 32) {
+      const uint32_t w = col[e];
+      if (depth[w] == level + 1) acc += bc_term(sv, sigma[w], delta[w]);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (lane == 0) delta[v] = delta[v] + acc;
+  }
+}
+
+// centrality += delta (delta[source] counted as 0), delta cleared for the next source
+__global__ void k_bc_accum(int64_t n, int64_t source, double *__restrict__ delta,
+                           double *__restrict__ cent) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const double d = v == source ? 0.0 : delta[v];
+    cent[v] = __dadd_rn(cent[v], d);
+    delta[v] = 0.0;
+  }
+}
+
+// blocked pull step with path counts on warp tiles: every row sums sigma over
+// its frontier in-neighbours (tiles.cuh); unvisited rows with a hit are
+// discovered and take the sum (forward_pull_step traversal.py:143-176)
+__global__ void __launch_bounds__(256)
+    k_bc_pull_tiles(const uint32_t *__restrict__ col, const uint32_t *__restrict__ rstart,
+                    const uint32_t *__restrict__ id_map_b, const uint32_t *__restrict__ tile_row,
+                    int64_t es, int64_t ee, int64_t t0, int64_t ntiles,
+                    const uint32_t *__restrict__ front_bits, const int32_t *__restrict__ depth,
+                    const double *__restrict__ sigma, uint8_t *__restrict__ next,
+                    double *__restrict__ sig_add) {
+  constexpr int V = kTileV;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nw) {
+    const int64_t abase = (t0 + t) * kTileT;
+    const uint4 *cp = reinterpret_cast<const uint4 *>(col + abase + lane * V);
+    const uint4 ca = __ldcs(cp), cb = __ldcs(cp + 1);
+    const uint32_t c[V] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+    const uint32_t fw = rstart[(abase >> 5) + (lane < 8 ? lane : 8)];
+    const uint32_t r0 = tile_row[t];
+    const int llo = es > abase ? (int)(es - abase) : 0;
+    const int lhi = ee - abase < kTileT ? (int)(ee - abase) : kTileT;
+    const TileBits tb = tile_bits(fw, llo, lhi, lane);
+    double s[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const uint32_t u = c[k];
+      s[k] = (((tb.vm >> k) & 1u) && ((front_bits[u >> 5] >> (u & 31)) & 1u)) ? sigma[u] : 0.0;
+    }
+    tile_reduce<double>(
+        s, tb, r0, lane, 0.0, [](double a, double b) { return a + b; },
+        [&](uint32_t row, double x, uint32_t) {
+          if (!(x > 0.0)) return;
+          const uint32_t v = id_map_b[row];
+          if (depth[v] != kInfDepth) return;
+          next[v] = 1;
+          atomicAdd(sig_add + v, x);
+        });
+  }
+}
+
+// commit a level with path counts: ascending queue slice, depth stamp,
+// sigma += sig_add, the next frontier bitmap and its out-degree sum
+__global__ void k_bc_commit(int64_t n, int32_t level, uint8_t *__restrict__ next,
+                            const uint32_t *__restrict__ pos, uint32_t *__restrict__ queue_out,
+                            int32_t *__restrict__ depth, double *__restrict__ sigma,
+                            double *__restrict__ sig_add, uint32_t *__restrict__ front_bits,
+                            const int64_t *__restrict__ ro, unsigned long long *__restrict__ deg_sum) {
+  __shared__ unsigned long long s_sum;
+  if (threadIdx.x == 0) s_sum = 0;
+  __syncthreads();
+  unsigned long long local = 0;
+  const int64_t nwords = (n + 31) >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nwords * 32;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + threadIdx.x;
+    bool f = false;
+    if (v < n) {
+      f = next[v] != 0;
+      if (f) {
+        queue_out[pos[v]] = (uint32_t)v;
+        depth[v] = level;
+        next[v] = 0;
+        sigma[v] = __dadd_rn(sigma[v], sig_add[v]);
+        sig_add[v] = 0.0;
+        local += (unsigned long long)(ro[v + 1] - ro[v]);
+      }
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && (v >> 5) < nwords) front_bits[v >> 5] = word;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xffffffffu, local, d);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_sum, local);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(deg_sum, s_sum);
+}
+
+__global__ void k_bc_seed(int64_t src, int32_t *depth, double *sigma, uint32_t *queue,
+                          uint32_t *bits) {
+  depth[src] = 0;
+  sigma[src] = 1.0;
+  queue[0] = (uint32_t)src;
+  bits[src >> 5] = 1u << (src & 31);
+}
+
+// dependency pass over per-level ascending vertex lists (levels[off[l]:off[l+1]])
+static void bc_backward_dev(gcb_ctx *ctx, const gcb_csr *g, const int32_t *depth,
+                            const double *sigma, const uint32_t *levels,
+                            const std::vector<int64_t> &off, bool exact, double *delta) {
+  const int64_t L = (int64_t)off.size() - 1;  // number of non-empty levels
+  for (int64_t l = L - 2; l >= 0; --l) {
+    const int64_t cnt = off[l + 1] - off[l];
+    if (!cnt) continue;
+    if (exact) {
+      k_bc_back_exact<<<grid_for(cnt, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          cnt, levels + off[l], (int32_t)l, g->ro.p, g->col.p, depth, sigma, delta);
+      after_launch(ctx, "k_bc_back_exact");
+    } else {
+      k_bc_back_warp<<<grid_for(cnt * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          cnt, levels + off[l], (int32_t)l, g->ro.p, g->col.p, depth, sigma, delta);
+      after_launch(ctx, "k_bc_back_warp");
+    }
+  }
+}
+
+// forward sweep with path counts; fills depth / sigma / per-level queues
+static void bc_forward_dev(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int64_t source, int mode,
+                           int64_t capacity, int64_t value_bytes, Frontier &F, int32_t *depth,
+                           double *sigma, double *sig_add, uint32_t *levels,
+                           std::vector<int64_t> &off) {
+  const int64_t n = g->n;
+  k_fill_i32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, kInfDepth, depth);
+  after_launch(ctx, "k_fill_i32");
+  GCB_CUDA(cudaMemsetAsync(sigma, 0, n * sizeof(double), ctx->stream));
+  GCB_CUDA(cudaMemsetAsync(F.bits.p, 0, ((n + 31) / 32 + 1) * sizeof(uint32_t), ctx->stream));
+  k_bc_seed<<<1, 1, 0, ctx->stream>>>(source, depth, sigma, levels, F.bits.p);
+  after_launch(ctx, "k_bc_seed");
+  uint64_t work;
+  {
+    int64_t *h = (int64_t *)ctx->pinned;
+    d2h(ctx, h, g->ro.p + source, 2);
+    sync(ctx);
+    work = (uint64_t)(h[1] - h[0]);
+  }
+  off.assign(1, 0);
+  off.push_back(1);
+  int64_t qoff = 0, qsize = 1;
+  int32_t level = 0;
+  while (qsize > 0) {
+    bool pull;
+    if (mode == GCB_BFS_FORCE_PUSH || !bg) pull = false;
+    else if (mode == GCB_BFS_FORCE_PULL) pull = true;
+    else pull = (unsigned __int128)work * (unsigned __int128)value_bytes > (unsigned __int128)capacity;
+    if (!pull) {
+      k_step_push<<<grid_for(qsize * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          qsize, levels + qoff, g->ro.p, g->col.p, depth, sigma, F.next.p, sig_add);
+      after_launch(ctx, "k_step_push");
+    } else {
+      for (int64_t b = 0; b < bg->B; ++b) {
+        const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+        if (!Lb) continue;
+        const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
+        k_bc_pull_tiles<<<grid_for(nt * 32, 256, (int64_t)ctx->num_sms * 8), 256, 0,
+                          ctx->stream>>>(bg->col.p, bg->rstart.p, bg->id_map.p + rs,
+                                         bg->tile_row.p + tb, bg->h_edge_starts[b],
+                                         bg->h_edge_starts[b + 1], bg->h_tile_t0[b], nt, F.bits.p,
+                                         depth, sigma, F.next.p, sig_add);
+        after_launch(ctx, "k_bc_pull_tiles");
+      }
+    }
+    k_flags_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, F.next.p, F.flags.p);
+    after_launch(ctx, "k_flags_u32");
+    GCB_CUDA(cudaMemsetAsync(F.flags.p + n, 0, sizeof(uint32_t), ctx->stream));
+    cub_exclusive_sum_u32(ctx, F.flags.p, F.pos.p, n + 1);
+    GCB_CUDA(cudaMemsetAsync(F.degsum.p, 0, sizeof(unsigned long long), ctx->stream));
+    k_bc_commit<<<grid_for(((n + 31) / 32) * 32, 256, (int64_t)ctx->num_sms * 8), 256, 0,
+                  ctx->stream>>>(n, level + 1, F.next.p, F.pos.p, levels + qoff + qsize, depth,
+                                 sigma, sig_add, F.bits.p, g->ro.p, F.degsum.p);
+    after_launch(ctx, "k_bc_commit");
+    uint32_t *h = (uint32_t *)ctx->pinned;
+    unsigned long long *hs = (unsigned long long *)((char *)ctx->pinned + 64);
+    d2h(ctx, h, F.pos.p + n, 1);
+    d2h(ctx, hs, F.degsum.p, 1);
+    sync(ctx);
+    qoff += qsize;
+    qsize = *h;
+    work = *hs;
+    ++level;
+    if (qsize) off.push_back(qoff + qsize);
+  }
+}
+
+__global__ void k_level_hist(int64_t n, const int32_t *__restrict__ depth,
+                             unsigned long long *__restrict__ hist, int32_t maxd) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = depth[v];
+    if (d >= 0 && d <= maxd) atomicAdd(hist + d, 1ull);
+  }
+}
+
+__global__ void k_depth_keys(int64_t n, const int32_t *__restrict__ depth, uint32_t *__restrict__ key,
+                             uint32_t *__restrict__ val) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    key[v] = (uint32_t)depth[v];  // INF_DEPTH sorts last
+    val[v] = (uint32_t)v;
+  }
+}
+
+__global__ void k_max_depth(int64_t n, const int32_t *__restrict__ depth, int *__restrict__ out) {
+  int mx = -1;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = depth[v];
+    if (d != kInfDepth && d > mx) mx = d;
+  }
+  atomicMax(out, mx);
+}
+
+}  // namespace gcb
+
+extern "C" int gcb_bc(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, const int64_t *sources_host,
+                      int64_t num_sources, int mode, int64_t capacity_bytes, int64_t value_bytes,
+                      uint32_t flags, double *centrality_host) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && centrality_host && (sources_host || num_sources == 0), "NULL argument");
+  GCB_REQUIRE(mode >= 0 && mode <= 2, "unknown direction mode");
+  DeviceGuard dg(ctx->device);
+  const int64_t n = g->n;
+  for (int64_t i = 0; i < num_sources; ++i)
+    GCB_REQUIRE(sources_host[i] >= 0 && sources_host[i] < n, "source %lld out of range",
+                (long long)sources_host[i]);
+  gcb_blocked *owned = nullptr;
+  gcb_blocked *bg = bg_pull;
+  try {
+    if (mode != GCB_BFS_FORCE_PUSH && !bg && n > 0) bg = default_pull_blocking(ctx, g, &owned);
+    if (bg) {
+      GCB_REQUIRE(bg->n == n && bg->direction == 0, "g_blocked must be a pull blocking of g");
+      ensure_row_bits(ctx, bg);
+    }
+    DArray<int32_t> depth(n ? n : 1);
+    DArray<double> sigma(n ? n : 1), sig_add(n ? n : 1), delta(n ? n : 1), cent(n ? n : 1);
+    DArray<uint32_t> levels(n ? n : 1);
+    Frontier F(n);
+    GCB_CUDA(cudaMemsetAsync(F.next.p, 0, n ? n : 1, ctx->stream));
+    GCB_CUDA(cudaMemsetAsync(sig_add.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));
+    GCB_CUDA(cudaMemsetAsync(delta.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));
+    GCB_CUDA(cudaMemsetAsync(cent.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));
+    const bool exact = flags & GCB_FLAG_EXACT;
+    std::vector<int64_t> off;
+    for (int64_t i = 0; i < num_sources; ++i) {
+      const int64_t s = sources_host[i];
+      bc_forward_dev(ctx, g, bg, s, mode, capacity_bytes, value_bytes, F, depth.p, sigma.p,
+                     sig_add.p, levels.p, off);
+      bc_backward_dev(ctx, g, depth.p, sigma.p, levels.p, off, exact, delta.p);
+      k_bc_accum<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, s, delta.p, cent.p);
+      after_launch(ctx, "k_bc_accum");
+    }
+    if (n) d2h(ctx, centrality_host, cent.p, n);
+    sync(ctx);
+  } catch (...) {
+    if (owned) gcb_blocked_destroy(owned);
+    throw;
+  }
+  if (owned) gcb_blocked_destroy(owned);
+  GCB_API_END
+}
+
+extern "C" int gcb_bc_backward(gcb_ctx *ctx, const gcb_csr *g, const int32_t *depth_host,
+                               const double *sigma_host, int64_t source, uint32_t flags,
+                               double *delta_host) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && depth_host && sigma_host && delta_host, "NULL argument");
+  DeviceGuard dg(ctx->device);
+  const int64_t n = g->n;
+  if (n == 0) return GCB_OK;
+  DArray<int32_t> depth(n);
+  DArray<double> sigma(n), delta(n);
+  DArray<uint32_t> k1(n), k2(n), v1(n), v2(n);
+  DArray<int> mx(1);
+  h2d(ctx, depth.p, depth_host, n);
+  h2d(ctx, sigma.p, sigma_host, n);
+  GCB_CUDA(cudaMemsetAsync(delta.p, 0, n * sizeof(double), ctx->stream));
+  GCB_CUDA(cudaMemsetAsync(mx.p, 0xff, sizeof(int), ctx->stream));  // -1
+  k_max_depth<<<grid_for(n, 256, 4096), 256, 0, ctx->stream>>>(n, depth.p, mx.p);
+  after_launch(ctx, "k_max_depth");
+  int maxd = -1;
+  d2h(ctx, &maxd, mx.p, 1);
+  sync(ctx);
+  if (maxd >= 0) {
+    // per-level ascending vertex lists: stable sort by depth (INF last)
+    k_depth_keys<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, depth.p, k1.p, v1.p);
+    after_launch(ctx, "k_depth_keys");
+    uint32_t *rk = nullptr, *rv = nullptr;
+    cub_sort_pairs_u32_u32(ctx, k1.p, k2.p, v1.p, v2.p, n, 32, &rk, &rv);
+    DArray<unsigned long long> hist(maxd + 1);
+    GCB_CUDA(cudaMemsetAsync(hist.p, 0, (maxd + 1) * sizeof(unsigned long long), ctx->stream));
+    k_level_hist<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, depth.p, hist.p, maxd);
+    after_launch(ctx, "k_level_hist");
+    std::vector<unsigned long long> h(maxd + 1);
+    d2h(ctx, h.data(), hist.p, maxd + 1);
+    sync(ctx);
+    std::vector<int64_t> off(1, 0);
+    for (int d = 0; d <= maxd; ++d) off.push_back(off.back() + (int64_t)h[d]);
+    bc_backward_dev(ctx, g, depth.p, sigma.p, rv, off, flags & GCB_FLAG_EXACT, delta.p);
+    const double zero = 0.0;
+    if (source >= 0 && source < n) h2d(ctx, delta.p + source, &zero, 1);
+  }
+  d2h(ctx, delta_host, delta.p, n);
+  sync(ctx);
+  GCB_API_END
+}

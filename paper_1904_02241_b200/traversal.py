@@ -24,11 +24,15 @@ __all__ = [
     "DirectionPolicy",
     "TraversalState",
     "BfsResult",
+    "BcResult",
     "SsspResult",
     "choose_direction",
     "forward_push_step",
     "forward_pull_step",
     "bfs",
+    "bc_backward",
+    "bc_single_source",
+    "bc",
     "sssp",
     "sample_sources",
 ]
@@ -81,6 +85,12 @@ class BfsResult:
     depth: np.ndarray
     levels: list
     directions: list
+
+
+@dataclasses.dataclass
+class BcResult:
+    centrality: np.ndarray
+    sources: np.ndarray
 
 
 @dataclasses.dataclass
@@ -167,6 +177,85 @@ def bfs(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
     levels = [verts[bounds[i]:bounds[i + 1]].copy() for i in range(nl.value)]
     directions = ["blocked-pull" if d else "push" for d in dirs[: ne.value]]
     return BfsResult(depth, levels, directions)
+
+
+def bc_backward(g: CsrGraph, depth: np.ndarray, sigma: np.ndarray, source: int, *,
+                exact: bool = True) -> np.ndarray:
+    """Dependency accumulation over the shortest-path DAG, deepest level first
+    (traversal.py:212-236): delta[v] = sum over out-edges v->w one level deeper
+    of (sigma[v]/sigma[w]) * (1 + delta[w]); delta[source] = 0.  ``exact``
+    keeps the reference's per-vertex CSR summation order (bit-identical)."""
+    n = g.num_vertices
+    d = np.ascontiguousarray(depth, dtype=np.int32)
+    sg = np.ascontiguousarray(sigma, dtype=np.float64)
+    if d.shape != (n,) or sg.shape != (n,):
+        raise ValueError("depth and sigma must have one entry per vertex")
+    delta = np.zeros(n, dtype=np.float64)
+    if n == 0:
+        return delta
+    h = g.device()
+    _lib.check(h.ctx._lib.gcb_bc_backward(h.ctx.handle, h.raw, _lib.ptr(d, _lib.P_i32),
+                                          _lib.ptr(sg, _lib.P_dbl), int(source),
+                                          _lib.FLAG_EXACT if exact else 0,
+                                          _lib.ptr(delta, _lib.P_dbl)), "bc_backward")
+    return delta
+
+
+def _forward(g, g_blocked, source, policy, accumulate_sigma):
+    """traversal.py:179-198 over the device level steps."""
+    _check_source(g, source)
+    n = g.num_vertices
+    state = TraversalState.initial(n, source)
+    levels = [state.frontier.copy()]
+    directions = []
+    if policy.mode != "force-push" and g_blocked is None:
+        g_blocked = partition_tocab(transpose(g), "pull", max(1, n // 8))
+    while state.frontier.size:
+        step_dir = choose_direction(g, state, policy)
+        directions.append(step_dir)
+        if step_dir == "push":
+            forward_push_step(g, state, accumulate_sigma)
+        else:
+            forward_pull_step(g_blocked, state, accumulate_sigma)
+        if state.frontier.size:
+            levels.append(state.frontier.copy())
+    return state, levels, directions
+
+
+def bc_single_source(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
+                     policy: DirectionPolicy = DirectionPolicy(), *, exact: bool = True):
+    """One source's forward sweep + dependency pass (traversal.py:239-254):
+    returns (delta, state, levels)."""
+    state, levels, _ = _forward(g, g_blocked, int(source), policy, True)
+    delta = bc_backward(g, state.depth, state.sigma, int(source), exact=exact)
+    return delta, state, levels
+
+
+def bc(g: CsrGraph, sources, g_blocked: BlockedGraph | None = None,
+       policy: DirectionPolicy = DirectionPolicy(), *, exact: bool = False) -> BcResult:
+    """Betweenness centrality accumulated over ``sources`` (traversal.py:257-278),
+    every source's forward sweep and dependency pass on the device.  Ordered
+    pairs; symmetrize the graph for the undirected definition.  ``exact``
+    selects the reference's summation order (bit-identical); the default warp
+    reductions differ by reassociation only."""
+    src = np.asarray(sources, dtype=np.int64)
+    n = g.num_vertices
+    for s in src:
+        _check_source(g, int(s))
+    h = g.device()
+    bgh = None
+    if policy.mode != "force-push":
+        if g_blocked is None:
+            g_blocked = partition_tocab(transpose(g), "pull", max(1, n // 8))
+        bgh = g_blocked.device()
+    cent = np.zeros(n, dtype=np.float64)
+    s64 = np.ascontiguousarray(src, dtype=np.int64)
+    _lib.check(h.ctx._lib.gcb_bc(h.ctx.handle, h.raw, None if bgh is None else bgh.raw,
+                                 _lib.ptr(s64, _lib.P_i64), s64.size, policy.code,
+                                 int(policy.cache_capacity_bytes), int(policy.value_bytes),
+                                 _lib.FLAG_EXACT if exact else 0, _lib.ptr(cent, _lib.P_dbl)),
+               "bc")
+    return BcResult(cent, src)
 
 
 def sssp(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,

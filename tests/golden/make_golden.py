@@ -13,9 +13,9 @@ import os
 
 import numpy as np
 from gcb.blocking import partition_tocab
-from gcb.graph import GraphGenSpec, from_edges, generate, transpose
+from gcb.graph import GraphGenSpec, from_edges, generate, symmetrize, transpose
 from gcb.kernels import PrParams, pr_baseline, pr_blocked, spmv, spmv_blocked
-from gcb.traversal import DirectionPolicy, bc_single_source, bfs
+from gcb.traversal import DirectionPolicy, bc, bc_backward, bc_single_source, bfs, sample_sources
 from gcb.util import result_checksum
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -79,6 +79,17 @@ def main():
         s[f"r10_bfs{srcv}_levels"] = np.concatenate(r.levels)
         s[f"r10_bfs{srcv}_levsizes"] = np.array([len(q) for q in r.levels])
         s[f"r10_bfs{srcv}_dirs"] = np.array([d == "blocked-pull" for d in r.directions])
+    # betweenness centrality (traversal.py:212-278) under all three policies
+    srcs = sample_sources(g, 8)
+    s["r10_bc_sources"] = srcs
+    for name, p in (("hyb", pol), ("push", DirectionPolicy("force-push")),
+                    ("pull", DirectionPolicy("force-pull"))):
+        s[f"r10_bc_{name}"] = bc(g, srcs, bgb if name != "push" else None, p).centrality
+    delta, st, _ = bc_single_source(g, 0, bgb, pol)
+    s["r10_bc0_delta"], s["r10_bc0_sigma"], s["r10_bc0_depth"] = delta, st.sigma, st.depth
+    gs = symmetrize(gen("rmat:8:4:3"))
+    s["r8s_ro"], s["r8s_col"] = gs.row_offsets, gs.col_indices
+    s["r8s_bc_all"] = bc(gs, np.arange(gs.num_vertices), policy=DirectionPolicy("force-push")).centrality
     np.savez_compressed(os.path.join(OUT, "small.npz"), **s)
 
     # --- rmat:16:16:1 checksums ----------------------------------------------
@@ -108,6 +119,9 @@ def main():
     c["bfs0_depth"] = result_checksum(bfs(g, 0, policy=DirectionPolicy("force-push")).depth)
     rh = bfs(g, 0, partition_tocab(gt, "pull", 2**12), DirectionPolicy("auto"))
     c["bfs0_hybrid_dirs"] = ["pull" if d == "blocked-pull" else "push" for d in rh.directions]
+    bsrc = sample_sources(g, 4)
+    c["bc4_sources"] = [int(x) for x in bsrc]
+    c["bc4_push"] = result_checksum(bc(g, bsrc, policy=DirectionPolicy("force-push")).centrality)
     with open(os.path.join(OUT, "checksums.json"), "w") as f:
         json.dump(c, f, indent=1, sort_keys=True)
     print("wrote", sorted(c))

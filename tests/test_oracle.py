@@ -185,3 +185,46 @@ def test_cc_oracle_vs_scipy():
     mins = np.full(lab.max() + 1, g.n, dtype=np.int64)
     np.minimum.at(mins, lab, np.arange(g.n))
     assert np.array_equal(got, mins[lab].astype(np.uint32))
+
+
+# --------------------------------------------------------------- betweenness
+def test_bc_golden(golden, r10):
+    g, _ = r10
+    srcs = golden["r10_bc_sources"]
+    got = orc.bc(g, srcs)
+    for name in ("push", "hyb", "pull"):  # the reference is direction-invariant here
+        assert np.array_equal(got, golden[f"r10_bc_{name}"]), name
+
+
+def test_bc_single_source_golden(golden, r10):
+    g, _ = r10
+    depth, sigma = orc.bfs_sigma(g, 0)
+    assert np.array_equal(depth, golden["r10_bc0_depth"])
+    assert np.array_equal(sigma, golden["r10_bc0_sigma"])
+    assert np.array_equal(orc.bc_backward(g, depth, sigma, 0), golden["r10_bc0_delta"])
+
+
+def test_bc_all_sources_symmetric(golden):
+    g = orc.Csr(len(golden["r8s_ro"]) - 1, len(golden["r8s_col"]), golden["r8s_ro"],
+                golden["r8s_col"])
+    assert np.array_equal(orc.bc(g, np.arange(g.n)), golden["r8s_bc_all"])
+
+
+def test_bc_rmat16_checksum(checksums, r16):
+    g, _ = r16
+    cent = orc.bc(g, np.array(checksums["bc4_sources"]))
+    assert orc.checksum(cent) == checksums["bc4_push"]
+
+
+def test_bc_kats():
+    # traversal tests: path middle, star centre, backward pass zeroes the source
+    def csr(n, src, dst):
+        return orc.from_edges(np.array(src, np.uint32), np.array(dst, np.uint32), n)
+    path3 = csr(3, [0, 1, 1, 2], [1, 0, 2, 1])  # symmetrize(path:3)
+    assert list(orc.bc(path3, np.arange(3))) == [0.0, 2.0, 0.0]
+    star = csr(5, [0, 0, 0, 0, 1, 2, 3, 4], [1, 2, 3, 4, 0, 0, 0, 0])
+    cent = orc.bc(star, np.arange(5))
+    assert cent[0] == 12.0 and (cent[1:] == 0.0).all()
+    path = csr(3, [0, 1], [1, 2])
+    delta = orc.bc_backward(path, np.array([0, 1, 2], np.int32), np.ones(3), 0)
+    assert list(delta) == [0.0, 1.0, 0.0]
