@@ -120,6 +120,14 @@ int gcb_csr_destroy(gcb_csr *g);
 /* partition_tocab blocking.py:204-253 on the device (bit-identical arenas). */
 int gcb_partition_tocab(gcb_ctx *ctx, const gcb_csr *g, int direction, int64_t width,
                         gcb_blocked **out);
+/* partition_cb blocking.py:256-286 (the conventional-blocking ablation): the
+ * same edge split as a pull TOCAB partition, but every block holds all n rows
+ * (identity id_map, empty rows included; row_starts[b] = b*n, a block's lro
+ * segment has n+1 entries).  pr_blocked / spmv_blocked on it run _cb_sums
+ * (kernels.py:350-364): a dense partial vector per block, merged in block order. */
+int gcb_partition_cb(gcb_ctx *ctx, const gcb_csr *g, int64_t width, gcb_blocked **out);
+/* Marks an uploaded pull blocking as cb-scheme (arenas already in that layout). */
+int gcb_blocked_mark_cb(gcb_ctx *ctx, gcb_blocked *bg);
 /* BlockedGraph(...) blocking.py:86-110 from host arenas (int64 lro converted
  * to per-block uint32 local offsets on the device). */
 int gcb_blocked_upload(gcb_ctx *ctx, int direction, int64_t width, int64_t n, int64_t m,

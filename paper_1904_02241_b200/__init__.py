@@ -13,6 +13,7 @@ from .blocking import (
     SubgraphBlock,
     block_stats,
     num_blocks_for,
+    partition_cb,
     partition_tocab,
     read_gcb,
     width_for_l2,

@@ -27,6 +27,7 @@ __all__ = [
     "BlockedGraph",
     "BlockStats",
     "partition_tocab",
+    "partition_cb",
     "block_stats",
     "num_blocks_for",
     "width_for_l2",
@@ -196,8 +197,10 @@ class BlockedGraph:
     # ---- device copy ----
     def device(self, ctx=None) -> "_lib.Handle":
         if self._dev is None:
-            if self.scheme != "tocab":
-                raise NotImplementedError("only the tocab scheme runs on the device")
+            if self.scheme not in ("tocab", "cb"):
+                raise ValueError(f"unknown blocking scheme {self.scheme!r}")
+            if self.scheme == "cb" and self.direction != "pull":
+                raise ValueError("the cb scheme is pull-only")
             ctx = ctx or _lib.context()
             a = {k: self._host[k] for k in self._ARENAS}
             for key in ("row_starts", "lro_arena", "edge_starts"):
@@ -212,6 +215,8 @@ class BlockedGraph:
                 _lib.ptr(a["edge_starts"], _lib.P_i64), _lib.ptr(a["col_arena"], _lib.P_u32),
                 _lib.ptr(a["weight_arena"], _lib.P_dbl), ctypes.byref(raw)), "blocked upload")
             self._dev = _lib.Handle(ctx, raw, "gcb_blocked_destroy")
+            if self.scheme == "cb":
+                _lib.check(ctx._lib.gcb_blocked_mark_cb(ctx.handle, raw), "cb layout")
         return self._dev
 
     @classmethod
@@ -266,6 +271,19 @@ def partition_tocab(g: CsrGraph, direction: str, width: int) -> BlockedGraph:
                                               0 if direction == "pull" else 1, int(width),
                                               ctypes.byref(raw)), "partition_tocab")
     return BlockedGraph._from_device(h.ctx, raw)
+
+
+def partition_cb(g: CsrGraph, width: int) -> BlockedGraph:
+    """Conventional blocking (blocking.py:256-286), the ablation of TOCAB:
+    the same edge split, but every block carries all n rows (identity row
+    map, empty rows included).  Pull only: pass the transposed graph."""
+    if int(width) < 1:
+        raise ValueError("width must be >= 1")
+    h = g.device()
+    raw = ctypes.c_void_p()
+    _lib.check(h.ctx._lib.gcb_partition_cb(h.ctx.handle, h.raw, int(width), ctypes.byref(raw)),
+               "partition_cb")
+    return BlockedGraph._from_device(h.ctx, raw, scheme="cb")
 
 
 # ---------------------------------------------------------------------------

@@ -140,6 +140,8 @@ constexpr int kMergeK = 2048;          // internal merge range width
 struct gcb_blocked {
   int device = 0;
   int direction = 0;  // 0 pull / 1 push
+  bool cb = false;    // conventional blocking (partition_cb, blocking.py:256-286): every
+                      // block holds all n rows (identity id_map, empty rows included)
   int64_t width = 0, n = 0, m = 0, B = 0, L = 0;
   bool weighted = false;
   std::vector<int64_t> h_row_starts, h_edge_starts;  // [B+1]
@@ -289,6 +291,10 @@ bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters);
 gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg);
 void permute_in(gcb_ctx *ctx, const gcb_blocked *bg, const double *x, double *x_new);
 void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, double *y);
+// partition.cu: conventional-blocking layout (the CB ablation)
+void to_cb_layout(gcb_ctx *ctx, gcb_blocked *bg);
+void cb_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights, bool exact,
+             double *out);
 // cub wrappers (cub_ops.cu)
 void cub_sort_keys_u64(gcb_ctx *ctx, uint64_t *keys, uint64_t *keys_alt, int64_t m, int end_bit,
                        uint64_t **result);

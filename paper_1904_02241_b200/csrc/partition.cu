@@ -298,6 +298,18 @@ namespace gcb {
 void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
   if (bg->derived) return;
   int64_t n = bg->n, B = bg->B;
+  if (bg->cb) {
+    // the CB kernels walk rows directly: out-degrees only
+    bg->deg.alloc(n);
+    GCB_CUDA(cudaMemsetAsync(bg->deg.p, 0, (n ? n : 1) * sizeof(uint32_t), ctx->stream));
+    if (bg->m) {
+      k_deg_pull<<<grid_for(bg->m, 256, 65536), 256, 0, ctx->stream>>>(bg->m, bg->col.p, bg->deg.p);
+      after_launch(ctx, "k_deg_pull");
+    }
+    sync(ctx);
+    bg->derived = true;
+    return;
+  }
   // out-degrees
   bg->deg.alloc(n);
   GCB_CUDA(cudaMemsetAsync(bg->deg.p, 0, (n ? n : 1) * sizeof(uint32_t), ctx->stream));
@@ -374,6 +386,130 @@ void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
   bg->derived = true;
 }
 
+// ---------------------------------------------------------------------------
+// Conventional blocking (partition_cb blocking.py:256-286; _cb_sums
+// kernels.py:350-364), kept as the ablation of TOCAB: the same edge split,
+// but every block carries all n rows (empty rows included) and its sums go
+// to a dense per-block vector that is merged in block order -- no row
+// compaction.  Results equal TOCAB's bit for bit (x + 0.0 == x), only the
+// memory traffic differs; profiles/ records both per edge.
+// ---------------------------------------------------------------------------
+__global__ void k_cb_counts(int64_t Lb, const uint32_t *__restrict__ lro_b,
+                            const uint32_t *__restrict__ id_map_b, uint32_t *__restrict__ cnt) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < Lb;
+       r += (int64_t)gridDim.x * blockDim.x)
+    cnt[id_map_b[r]] = lro_b[r + 1] - lro_b[r];
+}
+
+__global__ void k_cb_ids(int64_t n, int64_t B, uint32_t *__restrict__ id_map) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * B;
+       i += (int64_t)gridDim.x * blockDim.x)
+    id_map[i] = (uint32_t)(i % n);
+}
+
+void to_cb_layout(gcb_ctx *ctx, gcb_blocked *bg) {
+  GCB_REQUIRE(bg->direction == 0, "the cb scheme is pull-only");
+  const int64_t n = bg->n, B = bg->B;
+  DArray<uint32_t> lro((size_t)B * (n + 1) + 1), idm((size_t)(B * n ? B * n : 1)), cnt(n + 1);
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+    GCB_CUDA(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(uint32_t), ctx->stream));
+    if (Lb) {
+      k_cb_counts<<<grid_for(Lb, 256, 65536), 256, 0, ctx->stream>>>(Lb, bg->lro.p + rs + b,
+                                                                     bg->id_map.p + rs, cnt.p);
+      after_launch(ctx, "k_cb_counts");
+    }
+    cub_exclusive_sum_u32(ctx, cnt.p, lro.p + b * (n + 1), n + 1);
+  }
+  if (B * n) {
+    k_cb_ids<<<grid_for(B * n, 256, 65536), 256, 0, ctx->stream>>>(n, B, idm.p);
+    after_launch(ctx, "k_cb_ids");
+  }
+  bg->lro = std::move(lro);
+  bg->id_map = std::move(idm);
+  bg->L = B * n;
+  for (int64_t b = 0; b <= B; ++b) bg->h_row_starts[b] = b * n;
+  h2d(ctx, bg->row_starts.p, bg->h_row_starts.data(), B + 1);
+  sync(ctx);
+  bg->cb = true;
+}
+
+// one block's dense partial vector: exact = thread per row in storage order
+// (_gather_rows), fast = warp per row
+template <bool WGT>
+__global__ void k_cb_rows_exact(int64_t n, const uint32_t *__restrict__ lro_b,
+                                const uint32_t *__restrict__ col_b, const double *__restrict__ w_b,
+                                const double *__restrict__ vals, double *__restrict__ part) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (uint32_t e = lro_b[v]; e < lro_b[v + 1]; ++e)
+      acc = __dadd_rn(acc, WGT ? __dmul_rn(w_b[e], vals[col_b[e]]) : vals[col_b[e]]);
+    part[v] = acc;
+  }
+}
+
+template <bool WGT>
+__global__ void k_cb_rows_warp(int64_t n, const uint32_t *__restrict__ lro_b,
+                               const uint32_t *__restrict__ col_b, const double *__restrict__ w_b,
+                               const double *__restrict__ vals, double *__restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += nw) {
+    double acc = 0.0;
+    for (uint32_t e = lro_b[v] + lane; e < lro_b[v + 1]; e += 32)
+      acc += WGT ? w_b[e] * vals[col_b[e]] : vals[col_b[e]];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (lane == 0) part[v] = acc;
+  }
+}
+
+// sums = ((0 + part_0) + part_1) + ...  (the block-ordered merge of _cb_sums)
+__global__ void k_cb_merge(int64_t n, int64_t B, const double *__restrict__ part,
+                           double *__restrict__ out) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t b = 0; b < B; ++b) s = __dadd_rn(s, part[b * n + v]);
+    out[v] = s;
+  }
+}
+
+void cb_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights, bool exact,
+             double *out) {
+  const int64_t n = bg->n, B = bg->B;
+  const bool wgt = use_weights && bg->weighted;
+  bg->partials.ensure((size_t)(B * n ? B * n : 1));
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t es = bg->h_edge_starts[b];
+    const uint32_t *lro_b = bg->lro.p + b * (n + 1);
+    double *part = bg->partials.p + b * n;
+    const double *wb = wgt ? bg->w.p + es : nullptr;
+    ProfScope ps(ctx, 0);
+    if (exact) {
+      if (wgt)
+        k_cb_rows_exact<true><<<grid_for(n, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+            n, lro_b, bg->col.p + es, wb, vals, part);
+      else
+        k_cb_rows_exact<false><<<grid_for(n, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+            n, lro_b, bg->col.p + es, wb, vals, part);
+      after_launch(ctx, "k_cb_rows_exact");
+    } else {
+      if (wgt)
+        k_cb_rows_warp<true><<<grid_for(n * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+            n, lro_b, bg->col.p + es, wb, vals, part);
+      else
+        k_cb_rows_warp<false><<<grid_for(n * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+            n, lro_b, bg->col.p + es, wb, vals, part);
+      after_launch(ctx, "k_cb_rows_warp");
+    }
+  }
+  ProfScope ps(ctx, 2);
+  k_cb_merge<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, B, bg->partials.p, out);
+  after_launch(ctx, "k_cb_merge");
+}
+
 __global__ void k_narrow_lro(int64_t count, const int64_t *__restrict__ in,
                              uint32_t *__restrict__ out, unsigned int *__restrict__ bad) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
@@ -396,6 +532,32 @@ gcb_blocked *csr_compact_view(gcb_ctx *ctx, gcb_csr *g) {
 using namespace gcb;
 
 extern "C" {
+
+int gcb_partition_cb(gcb_ctx *ctx, const gcb_csr *g, int64_t width, gcb_blocked **out) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && out, "NULL argument");
+  DeviceGuard dg(ctx->device);
+  gcb_blocked *bg = partition_device(ctx, g, 0, width);
+  try {
+    to_cb_layout(ctx, bg);
+  } catch (...) {
+    delete bg;
+    throw;
+  }
+  *out = bg;
+  GCB_API_END
+}
+
+int gcb_blocked_mark_cb(gcb_ctx *ctx, gcb_blocked *bg) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg, "NULL argument");
+  GCB_REQUIRE(bg->direction == 0, "the cb scheme is pull-only");
+  for (int64_t b = 0; b <= bg->B; ++b)
+    GCB_REQUIRE(bg->h_row_starts[b] == b * bg->n, "cb blocks must hold all n rows");
+  GCB_REQUIRE(!bg->derived, "mark the scheme before the first computation");
+  bg->cb = true;
+  GCB_API_END
+}
 
 int gcb_partition_tocab(gcb_ctx *ctx, const gcb_csr *g, int direction, int64_t width,
                         gcb_blocked **out) {

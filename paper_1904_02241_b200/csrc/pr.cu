@@ -559,6 +559,12 @@ void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *v
                bool use_weights, uint32_t flags, int64_t block_only, double *out, bool accum) {
   ensure_derived(ctx, bg);
   const bool exact = flags & GCB_FLAG_EXACT;
+  if (bg->cb) {
+    GCB_REQUIRE(accum && block_only < 0 && vals && !vals32,
+                "the cb scheme supports whole-graph pull passes only");
+    cb_sums(ctx, bg, vals, use_weights, exact, out);  // partition.cu: the CB ablation
+    return;
+  }
   if (accum && !exact && vals && !vals32 && block_only < 0 && getenv("GCB_OLD_GATHER") == nullptr) {
     gather_accum(ctx, bg, vals, use_weights, flags, out);  // gather.cu: hot-staged path
     return;

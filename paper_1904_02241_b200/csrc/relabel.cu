@@ -76,7 +76,7 @@ __global__ void k_permute_out(int64_t n, const uint32_t *__restrict__ perm,
 bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters) {
   if (flags & (GCB_FLAG_EXACT | GCB_FLAG_NO_RELABEL)) return false;
   if (bg->direction != 0 || bg->m == 0 || bg->n >= (int64_t(1) << 32)) return false;
-  if (bg->is_relabeled) return false;
+  if (bg->is_relabeled || bg->cb) return false;
   const char *env = getenv("GCB_NO_RELABEL");
   if (env && env[0] && env[0] != '0') return false;
   if (bg->rl) return true;

@@ -224,8 +224,6 @@ def pr_blocked(bg: BlockedGraph, params: PrParams = PrParams(), k: int = DEFAULT
     ``k`` (merge range width) is validated; results are k-invariant bitwise.
     ``f32_values`` gathers an f32 copy of the contributions (sums stay f64).
     ``out`` (extension): float64[n] the ranks are written into and returned."""
-    if bg.scheme != "tocab":
-        raise NotImplementedError("the cb ablation scheme is not implemented on the device")
     if int(k) < 1:
         raise ValueError("range width k must be >= 1")
     n = bg.num_vertices
@@ -365,8 +363,6 @@ def spmv_blocked(bg: BlockedGraph, x, k: int = DEFAULT_RANGE_WIDTH, threads: int
                  exact: bool = False, out=None) -> np.ndarray:
     """Blocked y = A x over a TOCAB blocking (kernels.py:431-487).  ``out``
     (extension): float64[n] y is written into and returned."""
-    if bg.scheme != "tocab":
-        raise NotImplementedError("the cb ablation scheme is not implemented on the device")
     xv = _f64(x, bg.num_vertices)
     if int(k) < 1:
         raise ValueError("range width k must be >= 1")

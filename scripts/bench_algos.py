@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--spmv-scale", type=int, default=22)
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--only", default="spmv,bfs,sssp,cc")
+    ap.add_argument("--only", default="spmv,bfs,sssp,cc,bc")
     a = ap.parse_args()
     only = set(a.only.split(","))
     out = {}
@@ -50,7 +50,7 @@ def main():
         _, t = timed(lambda: gcb.spmv_blocked(bg, x, out=y), a.reps)
         out["spmv"]["ms_promoted"] = round(t * 1e3, 3)
         del gt, bg
-    if only & {"bfs", "sssp", "cc"}:
+    if only & {"bfs", "sssp", "cc", "bc"}:
         g = gcb.generate_rmat(a.scale, 16, 1)
         n, m = g.num_vertices, g.num_edges
         bgt = gcb.partition_tocab(gcb.transpose(g), "pull", max(1, n // 8))
@@ -74,6 +74,13 @@ def main():
             out["sssp"] = {"source": 0, "ms": round(t * 1e3, 2), "rounds": r.rounds,
                            "reached": int(reached.size), "directions": r.directions,
                            "gteps": round(int(deg[reached].sum()) / t / 1e9, 2)}
+        if "bc" in only:
+            src = gcb.sample_sources(g, 4)
+            for exact in (False, True):
+                r, t = timed(lambda: gcb.bc(g, src, bgt, exact=exact), 1)
+                out[f"bc_{'exact' if exact else 'fast'}"] = {
+                    "sources": [int(x) for x in src], "ms": round(t * 1e3, 2),
+                    "ms_per_source": round(t * 1e3 / len(src), 2)}
         if "cc" in only:
             r, t = timed(lambda: gcb.cc(g), a.reps)
             out["cc"] = {"ms": round(t * 1e3, 2), "components": r.num_components,

@@ -12,7 +12,7 @@ import json
 import os
 
 import numpy as np
-from gcb.blocking import partition_tocab
+from gcb.blocking import partition_cb, partition_tocab
 from gcb.graph import GraphGenSpec, from_edges, generate, symmetrize, transpose
 from gcb.kernels import PrParams, pr_baseline, pr_blocked, spmv, spmv_blocked
 from gcb.traversal import DirectionPolicy, bc, bc_backward, bc_single_source, bfs, sample_sources
@@ -79,6 +79,12 @@ def main():
         s[f"r10_bfs{srcv}_levels"] = np.concatenate(r.levels)
         s[f"r10_bfs{srcv}_levsizes"] = np.array([len(q) for q in r.levels])
         s[f"r10_bfs{srcv}_dirs"] = np.array([d == "blocked-pull" for d in r.directions])
+    # conventional blocking (the CB ablation, blocking.py:256-286)
+    for W in (64, 1000):
+        bcb = partition_cb(gt, W)
+        blocked_arrays(f"r10_cb{W}_", bcb, s)
+        s[f"r10_cb{W}_pr10"] = pr_blocked(bcb, PrParams(tol=0.0, max_iters=10)).ranks
+    s["r10w_cb64_spmv"] = spmv_blocked(partition_cb(gwt, 64), x)
     # betweenness centrality (traversal.py:212-278) under all three policies
     srcs = sample_sources(g, 8)
     s["r10_bc_sources"] = srcs

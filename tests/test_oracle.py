@@ -228,3 +228,14 @@ def test_bc_kats():
     path = csr(3, [0, 1], [1, 2])
     delta = orc.bc_backward(path, np.array([0, 1, 2], np.int32), np.ones(3), 0)
     assert list(delta) == [0.0, 1.0, 0.0]
+
+
+# ------------------------------------------------------- conventional blocking
+@pytest.mark.parametrize("W", [64, 1000])
+def test_partition_cb_golden(golden, r10, W):
+    _, gt = r10
+    bg = orc.partition_cb(gt, W)
+    for name in ("row_starts", "lro_arena", "id_map_arena", "edge_starts", "col_arena"):
+        assert np.array_equal(getattr(bg, name), golden[f"r10_cb{W}_{name}"]), name
+    # _cb_sums adds +0.0 for empty rows: ranks equal the TOCAB pull ones bitwise
+    assert np.array_equal(golden[f"r10_cb{W}_pr10"], golden[f"r10_pull{W}_pr10"])
