@@ -196,8 +196,8 @@ def workload_config(args, n, m):
         "iterations_per_step": args.iters, "damping": 0.85, "tol": 0.0,
         "direction": args.direction, "value_dtype": "f32" if args.f32_values else "f64",
         "l2": "inputs larger than L2 (col arena 4|E| bytes >> 126 MB)",
-        "parallelism": (f"destination shards x{args.gpus} (equal in-edges), NCCL all-gather of "
-                        "contributions" if args.gpus > 1 else "single GPU"),
+        "parallelism": (f"destination shards x{args.gpus} (equal in-edges), NCCL all_to_all of "
+                        "the contributions each shard reads" if args.gpus > 1 else "single GPU"),
     }
 
 
@@ -252,7 +252,8 @@ def run_ours(args):
             raise SystemExit("multi-GPU PageRank shards the pull direction")
         plan = parallel.ShardPlan(parallel.shard_ranges(src.row_offsets, world))
         engine = parallel.DeviceShard(src, *plan.owned(rank), args.width, flags)
-        runner = parallel.ShardedPageRank(engine, plan, rank, parallel.TorchExchange(plan, rank))
+        exchange = parallel.SparseExchange(plan, rank, engine.source_mask())
+        runner = parallel.ShardedPageRank(engine, plan, rank, exchange)
         n, m = src.num_vertices, src.num_edges
         bg = engine.bg
         del src

@@ -126,6 +126,9 @@ int gcb_partition_tocab(gcb_ctx *ctx, const gcb_csr *g, int direction, int64_t w
  * segment has n+1 entries).  pr_blocked / spmv_blocked on it run _cb_sums
  * (kernels.py:350-364): a dense partial vector per block, merged in block order. */
 int gcb_partition_cb(gcb_ctx *ctx, const gcb_csr *g, int64_t width, gcb_blocked **out);
+/* mask_dev[n] (device bytes) = 1 for every source the blocking's edges read:
+ * the per-rank need set of the sparse contribution exchange. */
+int gcb_blocked_source_mask(gcb_ctx *ctx, const gcb_blocked *bg, uint8_t *mask_dev);
 /* Marks an uploaded pull blocking as cb-scheme (arenas already in that layout). */
 int gcb_blocked_mark_cb(gcb_ctx *ctx, gcb_blocked *bg);
 /* BlockedGraph(...) blocking.py:86-110 from host arenas (int64 lro converted

@@ -68,6 +68,7 @@ SIGNATURES = {
     "gcb_partition_tocab": ([c_vp, c_vp, c_int, c_i64, PP], c_int),
     "gcb_partition_cb": ([c_vp, c_vp, c_i64, PP], c_int),
     "gcb_blocked_mark_cb": ([c_vp, c_vp], c_int),
+    "gcb_blocked_source_mask": ([c_vp, c_vp, c_vp], c_int),
     "gcb_blocked_upload": ([c_vp, c_int, c_i64, c_i64, c_i64, c_i64, P_i64, P_i64, P_u32, P_i64,
                             P_u32, P_dbl, PP], c_int),
     "gcb_blocked_info": ([c_vp, P_int, P_i64, P_i64, P_i64, P_i64, P_i64, P_int], c_int),

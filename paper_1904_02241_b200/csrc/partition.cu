@@ -510,6 +510,13 @@ void cb_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights
   after_launch(ctx, "k_cb_merge");
 }
 
+// mask[v] = 1 for every source the arena references (the sparse exchange plan)
+__global__ void k_mark_sources(int64_t m, const uint32_t *__restrict__ col, uint8_t *__restrict__ mask) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    mask[col[e]] = 1;
+}
+
 __global__ void k_narrow_lro(int64_t count, const int64_t *__restrict__ in,
                              uint32_t *__restrict__ out, unsigned int *__restrict__ bad) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
@@ -532,6 +539,19 @@ gcb_blocked *csr_compact_view(gcb_ctx *ctx, gcb_csr *g) {
 using namespace gcb;
 
 extern "C" {
+
+int gcb_blocked_source_mask(gcb_ctx *ctx, const gcb_blocked *bg, uint8_t *mask_dev) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && (mask_dev || bg->n == 0), "NULL argument");
+  DeviceGuard dg(ctx->device);
+  if (bg->n) GCB_CUDA(cudaMemsetAsync(mask_dev, 0, bg->n, ctx->stream));
+  if (bg->m) {
+    k_mark_sources<<<grid_for(bg->m, 256, 65536), 256, 0, ctx->stream>>>(bg->m, bg->col.p, mask_dev);
+    after_launch(ctx, "k_mark_sources");
+  }
+  sync(ctx);
+  GCB_API_END
+}
 
 int gcb_partition_cb(gcb_ctx *ctx, const gcb_csr *g, int64_t width, gcb_blocked **out) {
   GCB_API_BEGIN

@@ -9,7 +9,9 @@ full f64 contribution vector, and per iteration
 
     1. gathers its slab against the full contribution vector (device),
     2. updates ranks / contributions of its owned slice in place (device),
-    3. all-gathers the owned contribution slices over NCCL (NVLink),
+    3. exchanges contributions over NCCL (NVLink): SparseExchange sends each
+       rank only the sources its slab reads (all_to_all_single of packed f64,
+       ~4x fewer bytes than TorchExchange's padded all-gather at P=8),
     4. all-reduces the scalar L1 delta when tol > 0.
 
 One process per GPU; torch.distributed provides the communicator (NCCL on
@@ -29,7 +31,7 @@ from .blocking import BlockedGraph, partition_tocab
 from .graph import CsrGraph
 from .kernels import PrParams, PrResult
 
-__all__ = ["shard_ranges", "DeviceShard", "TorchExchange", "LoopbackExchange",
+__all__ = ["shard_ranges", "DeviceShard", "TorchExchange", "SparseExchange", "LoopbackExchange",
            "ShardedPageRank", "sharded_pagerank_virtual"]
 
 
@@ -114,6 +116,71 @@ class TorchExchange:
         return float(t.item())
 
 
+class SparseExchange:
+    """The sparse contribution exchange of SURVEY 8e: rank p receives only the
+    contributions its slab reads (at P=8 on R-MAT ~22-26% of all sources, so
+    ~4x fewer bytes than the all-gather).  The plan is built once: every rank
+    marks the sources its arena references, the per-owner index lists are
+    swapped with one all_to_all, and each iteration is then one index gather,
+    one all_to_all_single of packed f64 values and one index scatter.
+    Entries a rank never reads stay stale, which its gather cannot observe."""
+
+    def __init__(self, plan: ShardPlan, rank: int, needed, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.plan, self.rank, self.group = plan, rank, group
+        self.full = TorchExchange(plan, rank, group)  # for the final ranks gather
+        dev = needed.device
+        P = plan.parts
+        need = []
+        for q in range(P):
+            a, b = plan.owned(q)
+            if q == rank or b <= a:
+                need.append(torch.zeros(0, dtype=torch.int64, device=dev))
+            else:
+                need.append(torch.nonzero(needed[a:b]).flatten().to(torch.int64) + a)
+        recv_counts = torch.tensor([t.numel() for t in need], dtype=torch.int64, device=dev)
+        send_counts = torch.empty_like(recv_counts)
+        dist.all_to_all_single(send_counts, recv_counts, group=group)
+        self.recv_splits = recv_counts.tolist()
+        self.send_splits = send_counts.tolist()
+        self.recv_idx = torch.cat(need) if need else torch.zeros(0, dtype=torch.int64, device=dev)
+        self.send_idx = torch.empty(sum(self.send_splits), dtype=torch.int64, device=dev)
+        dist.all_to_all_single(self.send_idx, self.recv_idx, output_split_sizes=self.send_splits,
+                               input_split_sizes=self.recv_splits, group=group)
+        self._buf = {}
+
+    @property
+    def bytes_received(self) -> int:
+        return 8 * int(sum(self.recv_splits))
+
+    def _buffers(self, full):
+        import torch
+
+        key = (full.device, full.dtype)
+        if key not in self._buf:
+            self._buf[key] = (torch.empty(self.send_idx.numel(), dtype=full.dtype, device=full.device),
+                              torch.empty(self.recv_idx.numel(), dtype=full.dtype, device=full.device))
+        return self._buf[key]
+
+    def sync(self, full):
+        import torch
+        import torch.distributed as dist
+
+        send, recv = self._buffers(full)
+        torch.index_select(full, 0, self.send_idx, out=send)
+        dist.all_to_all_single(recv, send, output_split_sizes=self.recv_splits,
+                               input_split_sizes=self.send_splits, group=self.group)
+        full.index_copy_(0, self.recv_idx, recv)
+
+    def sync_full(self, full):
+        self.full.sync(full)
+
+    def allreduce_sum(self, x: float, device) -> float:
+        return self.full.allreduce_sum(x, device)
+
+
 class LoopbackExchange:
     """P virtual shards in one process (single-GPU validation of the sharded
     path): each shard has its own full vectors; sync copies owned slices."""
@@ -155,6 +222,16 @@ class DeviceShard:
                                                ctypes.c_void_p(self.deg.data_ptr())), "col counts")
         self.delta = torch.zeros(1, dtype=torch.float64, device=dev)
         self.device = dev
+
+    def source_mask(self):
+        """bool[n] on the device: the sources this shard's arena reads."""
+        import torch
+
+        mask = torch.zeros(self.n, dtype=torch.uint8, device=self.device)
+        _lib.check(self.ctx._lib.gcb_blocked_source_mask(self.ctx.handle, self.bg.device().raw,
+                                                         ctypes.c_void_p(mask.data_ptr())),
+                   "source mask")
+        return mask.bool()
 
     def init(self, contrib, ranks):
         _lib.check(self.ctx._lib.gcb_pr_shard_init(
@@ -200,7 +277,7 @@ class ShardedPageRank:
                     conv = True
                     break
         if gather_ranks:
-            self.exchange.sync(ranks)
+            getattr(self.exchange, "sync_full", self.exchange.sync)(ranks)
         return PrResult(ranks, it, conv)
 
 

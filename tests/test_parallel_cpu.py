@@ -58,6 +58,11 @@ class OracleShard:
         self.deg = np.bincount(gt.col, minlength=gt.n).astype(np.int64)
         self.device = torch.device("cpu")
 
+    def source_mask(self):
+        mask = torch.zeros(self.n, dtype=torch.bool)
+        mask[torch.from_numpy(self.col.astype(np.int64))] = True
+        return mask
+
     def init(self, contrib, ranks):
         r0 = 1.0 / self.n
         sl = slice(self.v0, self.v1)
@@ -82,7 +87,7 @@ class OracleShard:
         return torch.tensor([delta], dtype=torch.float64)
 
 
-def _worker(rank, world, port, scale, params, out_dir):
+def _worker(rank, world, port, scale, params, out_dir, sparse=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -90,7 +95,14 @@ def _worker(rank, world, port, scale, params, out_dir):
         gt = orc.rmat_transpose(scale, 8, 3, threads=1)
         plan = parallel.ShardPlan(parallel.shard_ranges(gt.row_offsets, world))
         eng = OracleShard(gt, *plan.owned(rank))
-        runner = parallel.ShardedPageRank(eng, plan, rank, parallel.TorchExchange(plan, rank))
+        ex = (parallel.SparseExchange(plan, rank, eng.source_mask()) if sparse
+              else parallel.TorchExchange(plan, rank))
+        if sparse:  # the plan sends each rank only what its slab reads
+            needed = eng.source_mask()
+            a, b = plan.owned(rank)
+            needed[a:b] = False
+            assert int(needed.sum()) == len(ex.recv_idx)
+        runner = parallel.ShardedPageRank(eng, plan, rank, ex)
         res = runner.run(PrParams(*params))
         np.save(os.path.join(out_dir, f"ranks{rank}.npy"), res.ranks.numpy())
         np.save(os.path.join(out_dir, f"meta{rank}.npy"), np.array([res.iterations,
@@ -105,10 +117,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("sparse", [False, True])
 @pytest.mark.parametrize("params", [(0.85, 0.0, 10), (0.85, 1e-4, 100)])
-def test_two_rank_sharded_pagerank_matches_oracle(tmp_path, params):
+def test_two_rank_sharded_pagerank_matches_oracle(tmp_path, params, sparse):
     scale = 11
-    mp.spawn(_worker, args=(2, _free_port(), scale, params, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), scale, params, str(tmp_path), sparse), nprocs=2,
+             join=True)
     gt = orc.rmat_transpose(scale, 8, 3)
     want = orc.pr_baseline(gt, "pull", damping=params[0], tol=params[1], max_iters=params[2])
     for rank in range(2):
@@ -121,3 +135,14 @@ def test_two_rank_sharded_pagerank_matches_oracle(tmp_path, params):
             # delta is a sum of per-rank partials, not numpy's pairwise sum:
             # the stop iteration may differ only at an exact tie
             assert abs(int(it) - want.iterations) <= 1 and bool(conv)
+
+
+def test_three_rank_sparse_exchange(tmp_path):
+    scale = 10
+    params = (0.85, 0.0, 10)
+    mp.spawn(_worker, args=(3, _free_port(), scale, params, str(tmp_path), True), nprocs=3,
+             join=True)
+    gt = orc.rmat_transpose(scale, 8, 3)
+    want = orc.pr_baseline(gt, "pull", damping=0.85, tol=0.0, max_iters=10)
+    for rank in range(3):
+        assert np.array_equal(np.load(tmp_path / f"ranks{rank}.npy"), want.ranks)
