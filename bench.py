@@ -333,7 +333,11 @@ def run_ours(args):
     if os.path.exists(prof_file):
         try:
             with open(prof_file) as fh:
-                traffic = json.load(fh).get("k_pull_hot_bytes_per_iteration")
+                tj = json.load(fh)
+            # only when the capture is of this very workload
+            if (tj.get("graph") == f"rmat:{args.scale}:{args.edge_factor}:{args.seed}"
+                    and tj.get("width") == args.width):
+                traffic = tj.get("k_pull_hot_bytes_per_iteration")
         except Exception:
             traffic = None
     roofline = {
