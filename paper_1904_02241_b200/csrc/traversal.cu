@@ -358,26 +358,62 @@ __global__ void k_cc_init(int64_t n, uint32_t *parent) {
     parent[v] = (uint32_t)v;
 }
 
-__global__ void k_cc_hook(int64_t n, const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
-                          uint32_t *parent) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = warp; u < n; u += nw) {
-    const int64_t s = ro[u], e = ro[u + 1];
-    for (int64_t k = s + lane; k < e; k += 32) {
-      uint32_t a = (uint32_t)u, b = col[k];
-      while (true) {
-        a = uf_find(parent, a);
-        b = uf_find(parent, b);
-        if (a == b) break;
-        const uint32_t hi = a > b ? a : b, lo = a > b ? b : a;
-        const uint32_t old = atomicCAS(&parent[hi], hi, lo);
-        if (old == hi) break;
-        a = old;  // hi got a new parent; retry from it
-        b = lo;
-      }
+// union of a and b (roots or not): hook the larger root under the smaller
+__device__ __forceinline__ void uf_union(uint32_t *parent, uint32_t a, uint32_t b) {
+  while (true) {
+    a = uf_find(parent, a);
+    b = uf_find(parent, b);
+    if (a == b) return;
+    const uint32_t hi = a > b ? a : b, lo = a > b ? b : a;
+    const uint32_t old = atomicCAS(&parent[hi], hi, lo);
+    if (old == hi) return;
+    a = old;
+    b = lo;
+  }
+}
+
+// Afforest-style sampling round: every vertex joins its r-th out-neighbour
+__global__ void k_cc_sample(int64_t n, int r, const int64_t *__restrict__ ro,
+                            const uint32_t *__restrict__ col, uint32_t *parent) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = ro[u] + r;
+    if (e < ro[u + 1]) uf_union(parent, (uint32_t)u, col[e]);
+  }
+}
+
+// pointer jumping: every vertex points at its root
+__global__ void k_cc_flatten(int64_t n, uint32_t *parent) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)v;
+    while (true) {
+      const uint32_t p = __ldcg(parent + x);
+      if (p == x) break;
+      x = p;
     }
+    parent[v] = x;
+  }
+}
+
+// every edge (u, v), edge-balanced (a hub row no longer serialises on one
+// warp); after the sampling rounds most endpoints already point straight at
+// the giant root, so the common case is two reads and no atomics
+__global__ void k_cc_src(int64_t n, const int64_t *__restrict__ ro, uint32_t *__restrict__ src) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nw)
+    for (int64_t k = ro[u] + lane; k < ro[u + 1]; k += 32) src[k] = (uint32_t)u;
+}
+
+__global__ void k_cc_edges(int64_t m, const uint32_t *__restrict__ src,
+                           const uint32_t *__restrict__ col, uint32_t *parent) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = src[e], v = col[e];
+    const uint32_t pu = __ldcg(parent + u), pv = __ldcg(parent + v);
+    if (pu == pv) continue;
+    uf_union(parent, pu, pv);
   }
 }
 
@@ -542,9 +578,21 @@ int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_c
   k_cc_init<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, parent.p);
   after_launch(ctx, "k_cc_init");
   if (g->m) {
-    k_cc_hook<<<grid_for(n * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-        n, g->ro.p, g->col.p, parent.p);
-    after_launch(ctx, "k_cc_hook");
+    // Afforest (Sutton et al.): two sampled neighbours per vertex, flatten,
+    // then the remaining edges with a cheap already-joined test
+    for (int r = 0; r < 2; ++r) {
+      k_cc_sample<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, r, g->ro.p, g->col.p,
+                                                                  parent.p);
+      after_launch(ctx, "k_cc_sample");
+      k_cc_flatten<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, parent.p);
+      after_launch(ctx, "k_cc_flatten");
+    }
+    DArray<uint32_t> src(g->m);
+    k_cc_src<<<grid_for(n * 32, 256, 65536), 256, 0, ctx->stream>>>(n, g->ro.p, src.p);
+    after_launch(ctx, "k_cc_src");
+    k_cc_edges<<<grid_for(g->m, 256, (int64_t)ctx->num_sms * 32), 256, 0, ctx->stream>>>(
+        g->m, src.p, g->col.p, parent.p);
+    after_launch(ctx, "k_cc_edges");
   }
   k_cc_compress<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, parent.p, cnt.p);
   after_launch(ctx, "k_cc_compress");
