@@ -141,6 +141,28 @@ def check(rc: int, what: str = ""):
     raise GcbError(text)
 
 
+_PIN_MIN_BYTES = 1 << 20
+
+
+def host_empty(n: int, dtype) -> np.ndarray:
+    """Result array for a device->host copy.  Large ones come from torch's
+    caching pinned-memory allocator (the copy runs at DMA speed -- a 67 MB
+    depth array to pageable memory took ~15 ms -- and the pinned block is
+    reused once the caller drops the array); small ones are plain numpy."""
+    dt = np.dtype(dtype)
+    nbytes = int(n) * dt.itemsize
+    if nbytes >= _PIN_MIN_BYTES:
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+                return t.numpy().view(dt)
+        except Exception:  # pragma: no cover - no driver: pageable memory
+            pass
+    return np.empty(int(n), dtype=dt)
+
+
 def ptr(a, typ):
     """Pointer into a contiguous numpy array (None -> NULL)."""
     if a is None:

@@ -29,7 +29,7 @@ class CcResult:
 def cc(g: CsrGraph) -> CcResult:
     """Edges are treated as undirected; no symmetrize() pass is needed."""
     h = g.device()
-    labels = np.empty(g.num_vertices, dtype=np.uint32)
+    labels = _lib.host_empty(g.num_vertices, np.uint32)
     count = ctypes.c_int64()
     _lib.check(h.ctx._lib.gcb_cc(h.ctx.handle, h.raw, _lib.ptr(labels, _lib.P_u32),
                                  ctypes.byref(count)), "cc")

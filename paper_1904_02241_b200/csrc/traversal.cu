@@ -18,25 +18,8 @@ namespace gcb {
 constexpr int32_t kInfDepth = INT32_MAX;
 constexpr int64_t kInfDist = INT64_MAX;
 
-// --------------------------------------------------------------------------
-// BFS push step (forward_push_step traversal.py:121-140): warp per frontier
-// vertex, lanes over out-edges; unvisited destinations get next[v] = 1.
-// --------------------------------------------------------------------------
-__global__ void k_bfs_push(int64_t qsize, const uint32_t *__restrict__ queue,
-                           const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
-                           const int32_t *__restrict__ depth, uint8_t *__restrict__ next) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < qsize; i += nw) {
-    const uint32_t u = queue[i];
-    const int64_t s = ro[u], e = ro[u + 1];
-    for (int64_t k = s + lane; k < e; k += 32) {
-      const uint32_t v = col[k];
-      if (depth[v] == kInfDepth) next[v] = 1;
-    }
-  }
-}
+// BFS push step (forward_push_step traversal.py:121-140): k_bfs_push_eb below,
+// one thread per frontier edge; unvisited destinations get next[v] = 1.
 
 // --------------------------------------------------------------------------
 // BFS blocked pull step (forward_pull_step traversal.py:143-176): per TOCAB
@@ -125,15 +108,62 @@ static gcb_blocked *default_pull_blocking(gcb_ctx *ctx, const gcb_csr *g,
 struct Frontier {
   DArray<uint8_t> next;
   DArray<uint32_t> flags, pos, bits;
+  DArray<uint32_t> qdeg, qoff;  // edge-balanced push: queue degrees and their prefix
   DArray<unsigned long long> degsum;
   explicit Frontier(int64_t n) {
     next.alloc(n ? n : 1);
     flags.alloc(n + 1);
     pos.alloc(n + 1);
     bits.alloc((n + 31) / 32 + 1);
+    qdeg.alloc(n + 1);
+    qoff.alloc(n + 1);
     degsum.alloc(1);
   }
 };
+
+// Edge-balanced push (a frontier holding one hub -- vertex 0 of rmat:24 has
+// 370K out-edges -- left a warp-per-vertex push on one warp for 3.4 ms):
+// qoff = exclusive prefix of the queue's out-degrees; one thread per frontier
+// edge finds its vertex by binary search (push levels are small by the
+// direction rule, <= capacity/value_bytes edges).
+__global__ void k_queue_degrees(int64_t qsize, const uint32_t *__restrict__ queue,
+                                const int64_t *__restrict__ ro, uint32_t *__restrict__ deg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= qsize;
+       i += (int64_t)gridDim.x * blockDim.x)
+    deg[i] = i < qsize ? (uint32_t)(ro[queue[i] + 1] - ro[queue[i]]) : 0u;
+}
+
+static void queue_offsets(gcb_ctx *ctx, const gcb_csr *g, const uint32_t *queue, int64_t qsize,
+                          Frontier &F) {
+  k_queue_degrees<<<grid_for(qsize + 1, 256, 65536), 256, 0, ctx->stream>>>(qsize, queue, g->ro.p,
+                                                                         F.qdeg.p);
+  after_launch(ctx, "k_queue_degrees");
+  cub_exclusive_sum_u32(ctx, F.qdeg.p, F.qoff.p, qsize + 1);
+}
+
+// largest i in [0, qsize) with qoff[i] <= idx
+__device__ __forceinline__ int64_t locate_edge(uint32_t idx, const uint32_t *__restrict__ qoff,
+                                               int64_t qsize) {
+  int64_t lo = 0, hi = qsize;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (qoff[mid] <= idx) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_bfs_push_eb(int64_t total, int64_t qsize, const uint32_t *__restrict__ queue,
+                              const uint32_t *__restrict__ qoff, const int64_t *__restrict__ ro,
+                              const uint32_t *__restrict__ col, const int32_t *__restrict__ depth,
+                              uint8_t *__restrict__ next) {
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = locate_edge((uint32_t)x, qoff, qsize);
+    const uint32_t v = col[ro[queue[i]] + (x - qoff[i])];
+    if (depth[v] == kInfDepth) next[v] = 1;
+  }
+}
 
 // flags -> queue slice at `out`; returns (count, degree sum) after a sync
 static void commit_level(gcb_ctx *ctx, const gcb_csr *g, Frontier &F, int32_t level,
@@ -203,9 +233,13 @@ static void bfs_run(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int64_t sou
     else pull = (unsigned __int128)work * (unsigned __int128)value_bytes > (unsigned __int128)capacity;
     dirs.push_back(pull ? 1 : 0);
     if (!pull) {
-      k_bfs_push<<<grid_for(qsize * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-          qsize, levels_dev + qoff, g->ro.p, g->col.p, depth_dev, F.next.p);
-      after_launch(ctx, "k_bfs_push");
+      if (work) {
+        queue_offsets(ctx, g, levels_dev + qoff, qsize, F);
+        k_bfs_push_eb<<<grid_for((int64_t)work, 256, (int64_t)ctx->num_sms * 32), 256, 0,
+                        ctx->stream>>>((int64_t)work, qsize, levels_dev + qoff, F.qoff.p, g->ro.p,
+                                       g->col.p, depth_dev, F.next.p);
+        after_launch(ctx, "k_bfs_push_eb");
+      }
     } else {
       for (int64_t b = 0; b < bg->B; ++b) {
         const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
@@ -235,24 +269,21 @@ static void bfs_run(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int64_t sou
 // transpose (min over frontier in-neighbours).  The fixpoint is the unique
 // shortest-distance vector, independent of direction and relaxation order.
 // --------------------------------------------------------------------------
-__global__ void k_sssp_push(int64_t qsize, const uint32_t *__restrict__ queue,
-                            const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
-                            const double *__restrict__ w, long long *__restrict__ dist,
-                            uint8_t *__restrict__ next) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < qsize; i += nw) {
+
+__global__ void k_sssp_push_eb(int64_t total, int64_t qsize, const uint32_t *__restrict__ queue,
+                               const uint32_t *__restrict__ qoff, const int64_t *__restrict__ ro,
+                               const uint32_t *__restrict__ col, const double *__restrict__ w,
+                               long long *__restrict__ dist, uint8_t *__restrict__ next) {
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = locate_edge((uint32_t)x, qoff, qsize);
     const uint32_t u = queue[i];
-    const long long du = dist[u];
-    const int64_t s = ro[u], e = ro[u + 1];
-    for (int64_t k = s + lane; k < e; k += 32) {
-      const uint32_t v = col[k];
-      const long long nd = du + (long long)w[k];
-      if (nd < dist[v]) {
-        const long long old = atomicMin(&dist[v], nd);
-        if (nd < old) next[v] = 1;
-      }
+    const int64_t k = ro[u] + (x - qoff[i]);
+    const uint32_t v = col[k];
+    const long long nd = dist[u] + (long long)w[k];
+    if (nd < dist[v]) {
+      const long long old = atomicMin(&dist[v], nd);
+      if (nd < old) next[v] = 1;
     }
   }
 }
@@ -527,9 +558,13 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
     else pull = (unsigned __int128)work * (unsigned __int128)value_bytes > (unsigned __int128)capacity_bytes;
     if (directions_host && r < max_rounds) directions_host[r] = pull ? 1 : 0;
     if (!pull) {
-      k_sssp_push<<<grid_for(qsize * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-          qsize, queue.p, g->ro.p, g->col.p, g->w.p, (long long *)dist.p, F.next.p);
-      after_launch(ctx, "k_sssp_push");
+      if (work) {
+        queue_offsets(ctx, g, queue.p, qsize, F);
+        k_sssp_push_eb<<<grid_for((int64_t)work, 256, (int64_t)ctx->num_sms * 32), 256, 0,
+                         ctx->stream>>>((int64_t)work, qsize, queue.p, F.qoff.p, g->ro.p, g->col.p,
+                                        g->w.p, (long long *)dist.p, F.next.p);
+        after_launch(ctx, "k_sssp_push_eb");
+      }
     } else {
       for (int64_t b = 0; b < bg->B; ++b) {
         const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
@@ -613,22 +648,21 @@ int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_c
 // ---------------------------------------------------------------------------
 namespace gcb {
 
-__global__ void k_step_push(int64_t qsize, const uint32_t *__restrict__ queue,
-                            const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
-                            const int32_t *__restrict__ depth, const double *__restrict__ sigma,
-                            uint8_t *__restrict__ next, double *__restrict__ sig_add) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < qsize; i += nw) {
+
+// edge-balanced form (see k_bfs_push_eb)
+__global__ void k_step_push_eb(int64_t total, int64_t qsize, const uint32_t *__restrict__ queue,
+                               const uint32_t *__restrict__ qoff, const int64_t *__restrict__ ro,
+                               const uint32_t *__restrict__ col, const int32_t *__restrict__ depth,
+                               const double *__restrict__ sigma, uint8_t *__restrict__ next,
+                               double *__restrict__ sig_add) {
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = locate_edge((uint32_t)x, qoff, qsize);
     const uint32_t u = queue[i];
-    const double su = sigma ? sigma[u] : 0.0;
-    for (int64_t k = ro[u] + lane; k < ro[u + 1]; k += 32) {
-      const uint32_t v = col[k];
-      if (depth[v] == kInfDepth) {
-        next[v] = 1;
-        if (sigma) atomicAdd(sig_add + v, su);
-      }
+    const uint32_t v = col[ro[u] + (x - qoff[i])];
+    if (depth[v] == kInfDepth) {
+      next[v] = 1;
+      if (sigma) atomicAdd(sig_add + v, sigma[u]);
     }
   }
 }
@@ -712,10 +746,16 @@ extern "C" int gcb_bfs_step(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull
   double *sg = sigma_host_or_null ? sigma.p : nullptr;
   if (direction == 0) {
     if (frontier_size) {
-      k_step_push<<<grid_for(frontier_size * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0,
-                    ctx->stream>>>(frontier_size, queue.p, g->ro.p, g->col.p, depth.p, sg, F.next.p,
-                                   sig_add.p);
-      after_launch(ctx, "k_step_push");
+      queue_offsets(ctx, g, queue.p, frontier_size, F);
+      uint32_t total = 0;
+      d2h(ctx, &total, F.qoff.p + frontier_size, 1);
+      sync(ctx);
+      if (total) {
+        k_step_push_eb<<<grid_for(total, 256, (int64_t)ctx->num_sms * 32), 256, 0, ctx->stream>>>(
+            total, frontier_size, queue.p, F.qoff.p, g->ro.p, g->col.p, depth.p, sg, F.next.p,
+            sig_add.p);
+        after_launch(ctx, "k_step_push_eb");
+      }
     }
   } else {
     gcb_blocked *bg = bg_pull;
@@ -957,9 +997,13 @@ static void bc_forward_dev(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int6
     else if (mode == GCB_BFS_FORCE_PULL) pull = true;
     else pull = (unsigned __int128)work * (unsigned __int128)value_bytes > (unsigned __int128)capacity;
     if (!pull) {
-      k_step_push<<<grid_for(qsize * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-          qsize, levels + qoff, g->ro.p, g->col.p, depth, sigma, F.next.p, sig_add);
-      after_launch(ctx, "k_step_push");
+      if (work) {
+        queue_offsets(ctx, g, levels + qoff, qsize, F);
+        k_step_push_eb<<<grid_for((int64_t)work, 256, (int64_t)ctx->num_sms * 32), 256, 0,
+                         ctx->stream>>>((int64_t)work, qsize, levels + qoff, F.qoff.p, g->ro.p,
+                                        g->col.p, depth, sigma, F.next.p, sig_add);
+        after_launch(ctx, "k_step_push_eb");
+      }
     } else {
       for (int64_t b = 0; b < bg->B; ++b) {
         const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;

@@ -197,7 +197,7 @@ def pr_baseline(g: CsrGraph, direction: str, params: PrParams = PrParams(),
     exact = deterministic or threads <= 1
     deg = None if out_degrees is None else np.ascontiguousarray(out_degrees, dtype=np.int64)
     h = g.device()
-    ranks = np.empty(n, dtype=np.float64)
+    ranks = _lib.host_empty(n, np.float64)
     iters, conv = _pr_call(h.ctx._lib.gcb_pr_baseline, h.ctx.handle, h.raw,
                            0 if direction == "pull" else 1, params.damping, params.tol,
                            params.max_iters, _flags(exact), _lib.ptr(deg, _lib.P_i64),
@@ -209,7 +209,7 @@ def _out_buffer(out, n: int) -> np.ndarray:
     """Caller-provided result buffer (e.g. pinned host memory, so the ranks
     come back by DMA) or a fresh array."""
     if out is None:
-        return np.empty(n, dtype=np.float64)
+        return _lib.host_empty(n, np.float64)
     if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == (n,)
             and out.flags.c_contiguous and out.flags.writeable):
         raise ValueError(f"out must be a writeable contiguous float64 array of length {n}")
@@ -351,7 +351,7 @@ def spmv(g: CsrGraph, x, direction: str = "pull", *, exact: bool = False) -> np.
     xv = _f64(x, g.num_vertices)
     if direction not in ("pull", "push"):
         raise ValueError(f"direction must be pull or push, got {direction!r}")
-    y = np.empty(g.num_vertices, dtype=np.float64)
+    y = _lib.host_empty(g.num_vertices, np.float64)
     h = g.device()
     _lib.check(h.ctx._lib.gcb_spmv(h.ctx.handle, h.raw, _lib.ptr(xv, _lib.P_dbl),
                                    0 if direction == "pull" else 1, _flags(exact),

@@ -162,8 +162,8 @@ def bfs(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
         if g_blocked is None:
             g_blocked = partition_tocab(transpose(g), "pull", max(1, n // 8))
         bgh = g_blocked.device()
-    depth = np.empty(n, dtype=np.int32)
-    verts = np.empty(n, dtype=np.uint32)
+    depth = _lib.host_empty(n, np.int32)
+    verts = _lib.host_empty(n, np.uint32)
     cap = n + 2
     sizes = np.zeros(cap, dtype=np.int64)
     dirs = np.zeros(cap, dtype=np.uint8)
@@ -248,7 +248,7 @@ def bc(g: CsrGraph, sources, g_blocked: BlockedGraph | None = None,
         if g_blocked is None:
             g_blocked = partition_tocab(transpose(g), "pull", max(1, n // 8))
         bgh = g_blocked.device()
-    cent = np.zeros(n, dtype=np.float64)
+    cent = _lib.host_empty(n, np.float64)
     s64 = np.ascontiguousarray(src, dtype=np.int64)
     _lib.check(h.ctx._lib.gcb_bc(h.ctx.handle, h.raw, None if bgh is None else bgh.raw,
                                  _lib.ptr(s64, _lib.P_i64), s64.size, policy.code,
@@ -279,7 +279,7 @@ def sssp(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
         if not g_blocked.weighted:
             raise ValueError("g_blocked must carry the edge weights")
         bgh = g_blocked.device()
-    dist = np.empty(n, dtype=np.int64)
+    dist = _lib.host_empty(n, np.int64)
     cap = 1 << 16
     dirs = np.zeros(cap, dtype=np.uint8)
     rounds = ctypes.c_int64()
