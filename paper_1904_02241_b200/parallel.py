@@ -35,8 +35,18 @@ __all__ = ["shard_ranges", "DeviceShard", "TorchExchange", "SparseExchange", "Lo
            "ShardedPageRank", "sharded_pagerank_virtual"]
 
 
-def shard_ranges(row_offsets, parts: int, align: int = 4) -> np.ndarray:
-    """Split rows into ``parts`` contiguous ranges with ~equal edge counts.
+# Cost of one owned vertex relative to one in-edge in a shard's step: the
+# update moves 44 B per owned vertex and short rows cost more per edge in the
+# gather.  Measured at rmat:24, P = 8 (scripts/shard_estimate.py, per-shard
+# step ms min/max): vertex_cost 0 (equal edges) 0.135/0.238, 2 0.148/0.201,
+# 4 0.161/0.180, 8 0.144/0.182 -- so cuts balance edges + 4 * vertices.
+VERTEX_COST = 4.0
+
+
+def shard_ranges(row_offsets, parts: int, align: int = 4,
+                 vertex_cost: float = VERTEX_COST) -> np.ndarray:
+    """Split rows into ``parts`` contiguous ranges of ~equal cost, cost =
+    in-edges + vertex_cost * rows (vertex_cost=0: equal edge counts).
 
     Boundaries are multiples of ``align`` (the update kernel's vector width)
     except the last, which is num_rows.  Returns int64[parts + 1]."""
@@ -44,11 +54,12 @@ def shard_ranges(row_offsets, parts: int, align: int = 4) -> np.ndarray:
     n = ro.size - 1
     if parts < 1:
         raise ValueError("parts must be >= 1")
-    m = int(ro[-1])
+    cost = ro.astype(np.float64) + float(vertex_cost) * np.arange(n + 1, dtype=np.float64)
+    total = float(cost[-1])
     cuts = [0]
     for r in range(1, parts):
-        target = (m * r) // parts
-        v = int(np.searchsorted(ro, target, side="left"))
+        target = total * r / parts
+        v = int(np.searchsorted(cost, target, side="left"))
         v = min(n, max(cuts[-1], (v // align) * align))
         cuts.append(v)
     cuts.append(n)

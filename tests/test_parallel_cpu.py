@@ -22,10 +22,19 @@ from paper_1904_02241_b200 import parallel
 from paper_1904_02241_b200.kernels import PrParams
 
 
+def test_shard_ranges_balance_cost():
+    g = orc.rmat_transpose(14, 16, 1)
+    vc = parallel.VERTEX_COST
+    for parts in (2, 4, 8):
+        cuts = parallel.shard_ranges(g.row_offsets, parts)
+        cost = np.diff(g.row_offsets[cuts]) + vc * np.diff(cuts)
+        assert cost.max() / cost.mean() < 1.05, cost
+
+
 def test_shard_ranges_equal_edges():
     g = orc.rmat_transpose(14, 16, 1)
     for parts in (1, 2, 3, 4, 8):
-        cuts = parallel.shard_ranges(g.row_offsets, parts)
+        cuts = parallel.shard_ranges(g.row_offsets, parts, vertex_cost=0.0)
         assert cuts[0] == 0 and cuts[-1] == g.n and len(cuts) == parts + 1
         assert (np.diff(cuts) >= 0).all()
         assert all(c % 4 == 0 for c in cuts[:-1])
