@@ -135,6 +135,7 @@ constexpr int kTileV = 8;              // edges per lane
 constexpr int kTileT = 32 * kTileV;    // edges per warp tile
 constexpr int64_t kColPad = 2 * kTileT; // padding so vector loads never fault
 constexpr int kMergeK = 2048;          // internal merge range width
+constexpr uint32_t kExactShort = 32;    // exact pull: longer rows get a warp each
 }  // namespace gcb
 
 struct gcb_blocked {
@@ -160,6 +161,8 @@ struct gcb_blocked {
   std::vector<int64_t> h_span_base;  // [B+1] prefix of carry-span starts
   gcb::DArray<uint32_t> span_tile;   // tile ids (global) of each row's first carry tile
   gcb::DArray<uint32_t> span_len;    // number of consecutive carry tiles of that row
+  std::vector<int64_t> h_long_base;  // [B+1] prefix of long rows per block
+  gcb::DArray<uint32_t> long_rows;   // local rows with > kExactShort edges (exact pull)
   int64_t R = 0;                     // merge ranges (ceil(n / kMergeK))
   gcb::DArray<int64_t> bounds;       // [B][R+1] arena positions per range
 

@@ -256,6 +256,20 @@ __global__ void k_span_len(int64_t nspans, int64_t ntiles, const uint32_t *__res
   }
 }
 
+__global__ void k_long_flags(int64_t Lb, const uint32_t *__restrict__ lro_b, uint32_t short_max,
+                             uint32_t *__restrict__ flag) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < Lb;
+       r += (int64_t)gridDim.x * blockDim.x)
+    flag[r] = lro_b[r + 1] - lro_b[r] > short_max ? 1u : 0u;
+}
+
+__global__ void k_compact_rows(int64_t Lb, const uint32_t *__restrict__ flag,
+                               const uint32_t *__restrict__ pos, uint32_t *__restrict__ out) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < Lb;
+       r += (int64_t)gridDim.x * blockDim.x)
+    if (flag[r]) out[pos[r]] = (uint32_t)r;
+}
+
 // bounds[b][j] = row_starts[b] + lower_bound(id_map_b, j*k), j in [0, R]
 __global__ void k_range_bounds(int64_t B, int64_t R, int64_t k, const int64_t *__restrict__ row_starts,
                                const uint32_t *__restrict__ id_map, int64_t *__restrict__ bounds) {
@@ -375,6 +389,47 @@ void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
       after_launch(ctx, "k_span_len");
     }
     for (int64_t b = 0; b <= B; ++b) bg->h_span_base[b] = hpos[b];
+  }
+  // long rows per block (exact pull: a warp each)
+  {
+    bg->h_long_base.assign(B + 1, 0);
+    std::vector<DArray<uint32_t>> parts;
+    DArray<uint32_t> lflag(bg->L + 1), lpos(bg->L + 1);
+    int64_t total = 0;
+    std::vector<int64_t> cnt(B, 0);
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+      if (Lb == 0) continue;
+      k_long_flags<<<grid_for(Lb, 256, 65536), 256, 0, ctx->stream>>>(Lb, bg->lro.p + rs + b,
+                                                                     kExactShort, lflag.p);
+      after_launch(ctx, "k_long_flags");
+      GCB_CUDA(cudaMemsetAsync(lflag.p + Lb, 0, sizeof(uint32_t), ctx->stream));
+      cub_exclusive_sum_u32(ctx, lflag.p, lpos.p, Lb + 1);
+      uint32_t c = 0;
+      d2h(ctx, &c, lpos.p + Lb, 1);
+      sync(ctx);
+      cnt[b] = c;
+      DArray<uint32_t> part(c ? c : 1);
+      if (c) {
+        k_compact_rows<<<grid_for(Lb, 256, 65536), 256, 0, ctx->stream>>>(Lb, lflag.p, lpos.p, part.p);
+        after_launch(ctx, "k_compact_rows");
+      }
+      parts.push_back(std::move(part));
+      total += c;
+    }
+    bg->long_rows.alloc(total ? total : 1);
+    int64_t at = 0, pi = 0;
+    for (int64_t b = 0; b < B; ++b) {
+      bg->h_long_base[b] = at;
+      const int64_t Lb = bg->h_row_starts[b + 1] - bg->h_row_starts[b];
+      if (Lb == 0) continue;
+      if (cnt[b])
+        GCB_CUDA(cudaMemcpyAsync(bg->long_rows.p + at, parts[pi].p, cnt[b] * sizeof(uint32_t),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+      at += cnt[b];
+      ++pi;
+    }
+    bg->h_long_base[B] = at;
   }
   // span tile ids were global; kernels subtract the block's tile base
   // merge bounds

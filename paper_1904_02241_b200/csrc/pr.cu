@@ -200,26 +200,82 @@ __global__ void k_fixup(int64_t nspans, const uint32_t *__restrict__ span_tile,
   }
 }
 
-// K2 exact: one thread per local row, storage order (kernels.py:155-170).
+// K2 exact: storage-order sums (kernels.py:155-170), bit-identical.  Rows of
+// up to kExactShort edges: one thread per row.  Longer rows (listed once per
+// block, ensure_derived) get a warp each: the lanes load and (if weighted)
+// multiply 32 edges in parallel, then every lane adds the 32 values in edge
+// order from the shuffles, so the rounding sequence is exactly the
+// sequential one.  (One thread per row left the 370K-edge hub row of rmat:24
+// on a single thread: 28 ms per exact iteration.)
+template <bool WGT, bool ACCUM>
+__device__ __forceinline__ void exact_store(double *out, const uint32_t *id_map_b, int64_t i, double s) {
+  if (ACCUM) {
+    double *p = out + id_map_b[i];
+    *p = __dadd_rn(*p, s);
+  } else {
+    out[i] = s;
+  }
+}
+
 template <bool WGT, bool ACCUM>
 __global__ void k_pull_exact(const uint32_t *__restrict__ col_b, const double *__restrict__ w_b,
                              const uint32_t *__restrict__ lro_b, const uint32_t *__restrict__ id_map_b,
-                             int64_t Lb, const double *__restrict__ vals, double *__restrict__ out) {
+                             int64_t Lb, const double *__restrict__ vals, double *__restrict__ out,
+                             uint32_t short_max) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Lb;
        i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t e0 = lro_b[i], e1 = lro_b[i + 1];
+    if (e1 - e0 > short_max) continue;  // k_pull_exact_long
     double s = 0.0;
-    const uint32_t e1 = lro_b[i + 1];
-    for (uint32_t e = lro_b[i]; e < e1; ++e) {
+    for (uint32_t e = e0; e < e1; ++e) {
       double x = vals[col_b[e]];
       if (WGT) x = __dmul_rn(w_b[e], x);
       s = __dadd_rn(s, x);
     }
-    if (ACCUM) {
-      double *p = out + id_map_b[i];
-      *p = __dadd_rn(*p, s);
-    } else {
-      out[i] = s;
+    exact_store<WGT, ACCUM>(out, id_map_b, i, s);
+  }
+}
+
+template <bool WGT, bool ACCUM>
+__global__ void k_pull_exact_long(const uint32_t *__restrict__ col_b, const double *__restrict__ w_b,
+                                  const uint32_t *__restrict__ lro_b,
+                                  const uint32_t *__restrict__ id_map_b,
+                                  const uint32_t *__restrict__ long_rows, int64_t nlong,
+                                  const double *__restrict__ vals, double *__restrict__ out) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nlong; j += nw) {
+    const uint32_t i = long_rows[j];
+    const uint32_t b0 = lro_b[i], b1 = lro_b[i + 1];
+    double acc = 0.0;
+    // 8 chunks of 32 edges per step: the 8 gathers of a lane are in flight
+    // together, then the 256 values are added in edge order
+    for (uint32_t base = b0; base < b1; base += 256) {
+      double x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t e = base + q * 32 + lane;
+        x[q] = 0.0;
+        if (e < b1) {
+          x[q] = vals[col_b[e]];
+          if (WGT) x[q] = __dmul_rn(w_b[e], x[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t cb = base + q * 32;
+        if (cb >= b1) break;
+        const int cnt = (int)(b1 - cb < 32u ? b1 - cb : 32u);
+        if (cnt == 32) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) acc = __dadd_rn(acc, __shfl_sync(FULL, x[q], k));
+        } else {
+          for (int k = 0; k < cnt; ++k) acc = __dadd_rn(acc, __shfl_sync(FULL, x[q], k));
+        }
+      }
     }
+    if (lane == 0) exact_store<WGT, ACCUM>(out, id_map_b, i, acc);
   }
 }
 
@@ -583,14 +639,22 @@ void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *v
       const unsigned g = grid_for(Lb, 256, (int64_t)ctx->num_sms * 16);
       const double *wb = wgt ? bg->w.p + es : nullptr;
       double *o = accum ? out : out + rs;
-      if (wgt && accum)
-        k_pull_exact<true, true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o);
-      else if (wgt)
-        k_pull_exact<true, false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o);
-      else if (accum)
-        k_pull_exact<false, true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o);
-      else
-        k_pull_exact<false, false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o);
+      const uint32_t *lr = bg->long_rows.p + bg->h_long_base[b];
+      const int64_t nl = bg->h_long_base[b + 1] - bg->h_long_base[b];
+      const unsigned gl = grid_for(nl * 32, 256, (int64_t)ctx->num_sms * 16);
+      if (wgt && accum) {
+        k_pull_exact<true, true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
+        if (nl) k_pull_exact_long<true, true><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+      } else if (wgt) {
+        k_pull_exact<true, false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
+        if (nl) k_pull_exact_long<true, false><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+      } else if (accum) {
+        k_pull_exact<false, true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
+        if (nl) k_pull_exact_long<false, true><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+      } else {
+        k_pull_exact<false, false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
+        if (nl) k_pull_exact_long<false, false><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+      }
       after_launch(ctx, "k_pull_exact");
       continue;
     }
