@@ -246,8 +246,9 @@ void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg) {
   ensure_row_bits(ctx, bg);
   int64_t K = hot_capacity(ctx);
   if (K > bg->width) K = bg->width;
+  if (bg->m == 0) K = 0;  // nothing to gather: no table (and no recode)
   bg->hot_k = K;
-  if (!bg->is_relabeled && K > 0 && bg->m > 0) {
+  if (!bg->is_relabeled && K > 0) {
     GCB_REQUIRE(n < (int64_t(1) << 31), "hot recode needs vertex ids below 2^31");
     bg->hot_ids.alloc(B * K);
     bg->hotval.alloc(B * K);
