@@ -196,7 +196,7 @@ def workload_config(args, n, m):
         "iterations_per_step": args.iters, "damping": 0.85, "tol": 0.0,
         "direction": args.direction, "value_dtype": "f32" if args.f32_values else "f64",
         "l2": "inputs larger than L2 (col arena 4|E| bytes >> 126 MB)",
-        "parallelism": (f"destination shards x{args.gpus} (equal in-edges), NCCL all_to_all of "
+        "parallelism": (f"destination shards x{args.gpus} (cuts balance in-edges + 4 x vertices), NCCL all_to_all of "
                         "the contributions each shard reads" if args.gpus > 1 else "single GPU"),
     }
 
@@ -251,7 +251,8 @@ def run_ours(args):
         if args.direction != "pull":
             raise SystemExit("multi-GPU PageRank shards the pull direction")
         plan = parallel.ShardPlan(parallel.shard_ranges(src.row_offsets, world))
-        engine = parallel.DeviceShard(src, *plan.owned(rank), args.width, flags)
+        # width 0: size each shard's blocks from the sources its slab reads
+        engine = parallel.DeviceShard(src, *plan.owned(rank), 0, flags)
         exchange = parallel.SparseExchange(plan, rank, engine.source_mask())
         runner = parallel.ShardedPageRank(engine, plan, rank, exchange)
         n, m = src.num_vertices, src.num_edges
@@ -378,6 +379,10 @@ def run_ours(args):
                          f"TOCAB W={args.width} graph, oracle/ C port with OpenMP, "
                          f"{c_s:.1f}s"}
 
+    cfg = workload_config(args, n, m)
+    if world > 1:
+        cfg["width"] = int(bg.width)  # rank 0's shard width (auto: DeviceShard._auto_width)
+        cfg["exchange_bytes_received_rank0"] = int(exchange.bytes_received)
     if rank == 0:
         line = {
             "metric": "PageRank GTEPS per iteration", "value": round(value, 3), "unit": "GTEPS",
@@ -385,7 +390,7 @@ def run_ours(args):
             "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic R-MAT generated on device (bit-exact with the reference)",
-            "config": workload_config(args, n, m),
+            "config": cfg,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
             "setup_s": round(setup_s, 2),

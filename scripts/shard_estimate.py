@@ -17,7 +17,7 @@ from paper_1904_02241_b200 import parallel  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 P = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-width = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 23
+width = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 0 = auto (DeviceShard)
 gt = gcb.generate_rmat(scale, 16, 1, transposed=True)
 n, m = gt.num_vertices, gt.num_edges
 vc = float(os.environ.get('VC', parallel.VERTEX_COST))
