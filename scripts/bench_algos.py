@@ -49,6 +49,35 @@ def main():
             gcb.spmv_blocked(bg, x, out=y)
         _, t = timed(lambda: gcb.spmv_blocked(bg, x, out=y), a.reps)
         out["spmv"]["ms_promoted"] = round(t * 1e3, 3)
+        # device-resident x / y (gcb_spmv_blocked_dev), CUDA events
+        import ctypes
+
+        import torch
+
+        from paper_1904_02241_b200 import _lib
+        h = bg.device()
+        ctx = h.ctx
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty_like(xd)
+        ctx.bind_torch_stream()
+
+        def dev():
+            _lib.check(ctx._lib.gcb_spmv_blocked_dev(ctx.handle, h.raw,
+                                                     ctypes.c_void_p(xd.data_ptr()), 0,
+                                                     ctypes.c_void_p(yd.data_ptr())))
+        for _ in range(3):
+            dev()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            dev()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        out["spmv"]["device_ms"] = round(ms, 4)
+        out["spmv"]["device_gteps"] = round(m / ms / 1e6, 1)
+        assert np.allclose(yd.cpu().numpy(), y, rtol=1e-12)
         del gt, bg
     if only & {"bfs", "sssp", "cc", "bc"}:
         g = gcb.generate_rmat(a.scale, 16, 1)
