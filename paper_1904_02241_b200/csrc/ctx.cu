@@ -125,6 +125,7 @@ int gcb_ctx_destroy(gcb_ctx *ctx) {
   ctx->scratch.release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
   GCB_API_END
 }

@@ -103,6 +103,7 @@ struct gcb_ctx {
   int64_t l2_bytes = 0, persist_max = 0, window_max = 0;
   int64_t launches = 0;
   void *pinned = nullptr;  // small pinned host staging (scalars)
+  cudaStream_t copy_stream = nullptr;  // host->device copies overlapped with kernels
   gcb::DArray<uint8_t> cub_tmp;
   gcb::DArray<uint8_t> scratch;  // general scratch
   // optional per-category kernel timing (gcb_ctx_set_profiling)
@@ -154,6 +155,7 @@ struct gcb_blocked {
 
   // ---- derived, built once by ensure_derived() ----
   bool derived = false;
+  bool deg_ready = false;            // deg already counted (overlapped with the upload)
   gcb::DArray<uint32_t> deg;         // out-degrees (kernels.py:324-330)
   std::vector<int64_t> h_tile_t0;    // first absolute tile id per block
   std::vector<int64_t> h_tile_base;  // [B+1] prefix of tiles per block

@@ -324,10 +324,10 @@ void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
     bg->derived = true;
     return;
   }
-  // out-degrees
-  bg->deg.alloc(n);
-  GCB_CUDA(cudaMemsetAsync(bg->deg.p, 0, (n ? n : 1) * sizeof(uint32_t), ctx->stream));
-  if (bg->m) {
+  // out-degrees (unless counted while the arena was uploaded)
+  if (!bg->deg_ready) bg->deg.alloc(n);
+  if (!bg->deg_ready) GCB_CUDA(cudaMemsetAsync(bg->deg.p, 0, (n ? n : 1) * sizeof(uint32_t), ctx->stream));
+  if (bg->m && !bg->deg_ready) {
     if (bg->direction == 0) {
       k_deg_pull<<<grid_for(bg->m, 256, 65536), 256, 0, ctx->stream>>>(bg->m, bg->col.p, bg->deg.p);
       after_launch(ctx, "k_deg_pull");
@@ -695,7 +695,43 @@ int gcb_blocked_upload(gcb_ctx *ctx, int direction, int64_t width, int64_t n, in
       GCB_REQUIRE(hbad == 0, "local row offset out of the 32-bit range");
     }
     h2d(ctx, bg->id_map.p, id_map_host, L);
-    h2d(ctx, bg->col.p, col_arena_host, m);
+    // col (the bulk of the bytes): for a pull blocking from pinned memory the
+    // copy is chunked on a second stream and the out-degree count
+    // (kernels.py:324-330) runs on each chunk as it lands, hidden behind the
+    // transfer (2.9 ms of the e2e step at rmat:24 otherwise)
+    cudaPointerAttributes pa;
+    const bool pinned_col = m > 0 && cudaPointerGetAttributes(&pa, col_arena_host) == cudaSuccess &&
+                            pa.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();
+    if (direction == 0 && pinned_col && !bg->cb) {
+      if (!ctx->copy_stream)
+        GCB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      bg->deg.alloc(n);
+      GCB_CUDA(cudaMemsetAsync(bg->deg.p, 0, (n ? n : 1) * sizeof(uint32_t), ctx->stream));
+      // the copy stream starts after the allocations / memsets above
+      cudaEvent_t ready;
+      GCB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      GCB_CUDA(cudaEventRecord(ready, ctx->stream));
+      GCB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
+      cudaEventDestroy(ready);
+      const int64_t chunk = int64_t(16) << 20;  // 64 MB of col per step
+      for (int64_t off = 0; off < m; off += chunk) {
+        const int64_t cnt = m - off < chunk ? m - off : chunk;
+        GCB_CUDA(cudaMemcpyAsync(bg->col.p + off, col_arena_host + off, cnt * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, ctx->copy_stream));
+        cudaEvent_t ev;
+        GCB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        GCB_CUDA(cudaEventRecord(ev, ctx->copy_stream));
+        GCB_CUDA(cudaStreamWaitEvent(ctx->stream, ev, 0));
+        cudaEventDestroy(ev);  // released once the wait is satisfied
+        k_deg_pull<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(cnt, bg->col.p + off,
+                                                                       bg->deg.p);
+        after_launch(ctx, "k_deg_pull");
+      }
+      bg->deg_ready = true;
+    } else {
+      h2d(ctx, bg->col.p, col_arena_host, m);
+    }
     if (bg->weighted) {
       bg->w.alloc(m + kColPad);
       h2d(ctx, bg->w.p, weight_arena_host_or_null, m);
