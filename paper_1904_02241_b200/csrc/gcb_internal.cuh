@@ -284,6 +284,7 @@ void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out);
 // gather.cu: fast pull gather accumulating into a dense vector (hot staging)
 void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg);
 void ensure_row_bits(gcb_ctx *ctx, gcb_blocked *bg);  // rstart only (tiles.cuh kernels)
+void ensure_push_exec(gcb_ctx *ctx, gcb_blocked *bg, int64_t hot_slots);  // push hot destinations
 void gather_accum(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights,
                   uint32_t flags, double *out);
 void cub_sort_pairs_desc_u32_u32(gcb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,

@@ -34,6 +34,7 @@ namespace gcb {
 }  // namespace gcb
 
 #include "ldst.cuh"
+#include "tiles.cuh"
 
 namespace gcb {
 
@@ -461,70 +462,121 @@ static void launch_update(gcb_ctx *ctx, bool exact, int64_t n, double base, doub
 // destination range (L2-resident); exact: one thread per block walks its
 // edges in storage order (np.bincount order, kernels.py:290-296).
 // ---------------------------------------------------------------------------
+// Push scatter on warp tiles with the row-start bitmap (tiles.cuh): the
+// values of the tile's first 32 source rows are fetched by the lanes up front
+// (one id_map + one vals load each, overlapped) and each edge takes its row's
+// value by shuffle; the loop of k_push_tiles reloaded id_map -> vals on every
+// row change (ncu: 55% long-scoreboard stalls, 11% issue).  Destinations are
+// accumulated with f64 RED into the block's (L2-resident) range.
 template <bool WGT>
-__global__ void __launch_bounds__(kWarps * 32)
-    k_push_tiles(const uint32_t *__restrict__ col, const double *__restrict__ w,
-                 const uint32_t *__restrict__ lro_b, const uint32_t *__restrict__ tile_row,
-                 int64_t es, int64_t ee, int64_t t0, int64_t ntiles, uint32_t Lb,
-                 const uint32_t *__restrict__ id_map_b, const double *__restrict__ vals,
-                 double *__restrict__ sums) {
+__global__ void __launch_bounds__(256)
+    k_push_bits(const uint32_t *__restrict__ col, const double *__restrict__ w,
+                const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ tile_row,
+                int64_t es, int64_t ee, int64_t t0, int64_t ntiles, uint32_t Lb,
+                const uint32_t *__restrict__ id_map_b, const double *__restrict__ vals,
+                double *__restrict__ sums) {
   constexpr int V = kTileV, T = kTileT;
-  __shared__ uint32_t s_ends[kWarps][T + 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t *ends = s_ends[wid];
-  const uint64_t pol_stream = policy_evict_first();
   const unsigned FULL = 0xffffffffu;
-  for (int64_t t = (int64_t)blockIdx.x * kWarps + wid; t < ntiles;
-       t += (int64_t)gridDim.x * kWarps) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol_stream = policy_evict_first();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nw) {
     const int64_t abase = (t0 + t) * T;
-    const int64_t lbase = abase - es;
-    const int64_t llo = lbase > 0 ? lbase : 0;
-    const int64_t lhi = (lbase + T < ee - es) ? lbase + T : ee - es;
-    const uint32_t r0 = tile_row[t];
     uint32_t c[V];
-    {
-      const uint4 *cp = reinterpret_cast<const uint4 *>(col + abase + lane * V);
-      uint4 a = ld_stream_u4(cp, pol_stream), b = ld_stream_u4(cp + 1, pol_stream);
-      c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
-      c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+    ld_stream_u32x8(col + abase + lane * V, pol_stream, c);
+    const uint32_t fw = rstart[(abase >> 5) + (lane < 8 ? lane : 8)];
+    const uint32_t r0 = tile_row[t];
+    const double rv = r0 + lane < Lb ? vals[id_map_b[r0 + lane]] : 0.0;
+    double ww[V];
+    if (WGT) {
+      ld_stream_f64x4(w + abase + lane * V, pol_stream, ww);
+      ld_stream_f64x4(w + abase + lane * V + 4, pol_stream, ww + 4);
     }
-    int nload = 0;
-    while (true) {
-      const uint32_t idx = r0 + 1 + nload + lane;
-      const uint32_t e = idx <= Lb ? lro_b[idx] : 0xffffffffu;
-      ends[nload + lane] = e;
-      const unsigned below = __ballot_sync(FULL, e < (uint32_t)lhi);
-      nload += 32;
-      if (below != FULL || nload >= T) break;
-    }
-    __syncwarp();
-    const int64_t q0 = lbase + (int64_t)lane * V;
-    const int64_t qf = q0 > llo ? q0 : llo;
-    if ((qf < lhi) && (q0 + V > llo)) {
-      int lo = 0, hi = nload;
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if ((int64_t)ends[mid] > qf) hi = mid;
-        else lo = mid + 1;
-      }
-      int j = lo;
-      uint32_t endj = ends[j];
-      double x = vals[id_map_b[r0 + j]];
+    const int llo = es > abase ? (int)(es - abase) : 0;
+    const int lhi = ee - abase < T ? (int)(ee - abase) : T;
+    const TileBits tb = tile_bits(fw, llo, lhi, lane);
+    // exclusive prefix of row starts over lanes -> the row of the lane's first edge
+    const int cnt = __popc(tb.bits);
+    int incl = cnt;
 #pragma unroll
-      for (int k = 0; k < V; ++k) {
-        const int64_t q = q0 + k;
-        if (q < llo || q >= lhi) continue;
-        if ((uint32_t)q >= endj) {
-          ++j;
-          endj = ends[j];
-          x = vals[id_map_b[r0 + j]];
-        }
-        double y = x;
-        if (WGT) y = __dmul_rn(w[abase + lane * V + k], x);
-        atomicAdd(sums + c[k], y);
-      }
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
     }
-    __syncwarp();
+    const int kf = tb.vm ? __ffs(tb.vm) - 1 : 0;
+    uint32_t rr = (uint32_t)(incl - cnt) + ((tb.bits >> kf) & 1u);  // row - r0
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      if (k > kf && ((tb.bits >> k) & 1u)) ++rr;
+      double x = __shfl_sync(FULL, rv, rr & 31);
+      if (!((tb.vm >> k) & 1u)) continue;
+      if (rr >= 32) x = vals[id_map_b[r0 + rr]];
+      if (WGT) x = __dmul_rn(ww[k], x);
+      atomicAdd(sums + c[k], x);
+    }
+  }
+}
+
+// Push scatter with hub destinations accumulated in shared memory: the
+// arena is recoded (ensure_push_exec) so an edge into one of the block's top
+// in-degree destinations carries 0x80000000 | slot; those adds go to the
+// CTA's accumulator (shared-memory atomic) and every CTA flushes its
+// non-zero slots with one global RED each at the end.
+template <bool WGT>
+__global__ void __launch_bounds__(1024, 1)
+    k_push_hot(const uint32_t *__restrict__ xcol, const double *__restrict__ w,
+               const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ tile_row,
+               int64_t es, int64_t ee, int64_t t0, int64_t ntiles, uint32_t Lb,
+               const uint32_t *__restrict__ id_map_b, const uint32_t *__restrict__ hot_ids_b,
+               int hot, const double *__restrict__ vals, double *__restrict__ sums) {
+  constexpr int V = kTileV, T = kTileT;
+  constexpr uint32_t kHot = 0x80000000u;
+  extern __shared__ double s_acc[];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol_stream = policy_evict_first();
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) s_acc[i] = 0.0;
+  __syncthreads();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nw) {
+    const int64_t abase = (t0 + t) * T;
+    uint32_t c[V];
+    ld_stream_u32x8(xcol + abase + lane * V, pol_stream, c);
+    const uint32_t fw = rstart[(abase >> 5) + (lane < 8 ? lane : 8)];
+    const uint32_t r0 = tile_row[t];
+    const double rv = r0 + lane < Lb ? vals[id_map_b[r0 + lane]] : 0.0;
+    double ww[V];
+    if (WGT) {
+      ld_stream_f64x4(w + abase + lane * V, pol_stream, ww);
+      ld_stream_f64x4(w + abase + lane * V + 4, pol_stream, ww + 4);
+    }
+    const int llo = es > abase ? (int)(es - abase) : 0;
+    const int lhi = ee - abase < T ? (int)(ee - abase) : T;
+    const TileBits tb = tile_bits(fw, llo, lhi, lane);
+    const int cnt = __popc(tb.bits);
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const int kf = tb.vm ? __ffs(tb.vm) - 1 : 0;
+    uint32_t rr = (uint32_t)(incl - cnt) + ((tb.bits >> kf) & 1u);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      if (k > kf && ((tb.bits >> k) & 1u)) ++rr;
+      double x = __shfl_sync(FULL, rv, rr & 31);
+      if (!((tb.vm >> k) & 1u)) continue;
+      if (rr >= 32) x = vals[id_map_b[r0 + rr]];
+      if (WGT) x = __dmul_rn(ww[k], x);
+      if (c[k] & kHot) atomicAdd(s_acc + (c[k] & ~kHot), x);
+      else atomicAdd(sums + c[k], x);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) {
+    const double v = s_acc[i];
+    if (v != 0.0) atomicAdd(sums + hot_ids_b[i], v);
   }
 }
 
@@ -694,9 +746,23 @@ void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out) {
   after_launch(ctx, "k_merge");
 }
 
+// Hub accumulator slots per block (f64 in shared memory).  rmat:24 push,
+// ms per iteration: none 3.69, 1K 1.75, 4K 1.48, 16K 1.28, 24K 1.07, 27K 1.07
+// -- REDs need no L1 staging, so unlike the pull gather the table can take
+// most of the shared memory.
+static int64_t push_hot_slots(gcb_ctx *ctx) {
+  int optin = 0;
+  GCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const char *env = getenv("GCB_PUSH_HOT");
+  int64_t K = env ? atoll(env) : 24576;
+  const int64_t cap = ((int64_t)optin - 1024) / 8;
+  return K < cap ? K : cap;
+}
+
 void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sums, bool use_weights,
                   uint32_t flags, int64_t block_only) {
   ensure_derived(ctx, bg);
+  if (!(flags & GCB_FLAG_EXACT)) ensure_push_exec(ctx, bg, push_hot_slots(ctx));
   const bool wgt = use_weights && bg->weighted;
   if (flags & GCB_FLAG_EXACT) {
     if (bg->B == 0) return;
@@ -719,16 +785,37 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
     if (Lb == 0) continue;
     const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
     const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
-    const unsigned g = tile_grid(ctx, nt);
+    if (bg->hot_k > 0) {
+      const int hot = (int)bg->hot_k;
+      const size_t smem = (size_t)hot * sizeof(double);
+      static size_t done = 0;
+      if (smem > done) {
+        GCB_CUDA(cudaFuncSetAttribute(k_push_hot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GCB_CUDA(cudaFuncSetAttribute(k_push_hot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        done = smem;
+      }
+      const unsigned gh = grid_for(nt * 32, 1024, (int64_t)ctx->num_sms);
+      if (wgt)
+        k_push_hot<true><<<gh, 1024, smem, ctx->stream>>>(
+            bg->xcol.p, bg->w.p, bg->rstart.p, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
+            (uint32_t)Lb, bg->id_map.p + rs, bg->hot_ids.p + b * bg->hot_k, hot, vals, sums);
+      else
+        k_push_hot<false><<<gh, 1024, smem, ctx->stream>>>(
+            bg->xcol.p, nullptr, bg->rstart.p, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
+            (uint32_t)Lb, bg->id_map.p + rs, bg->hot_ids.p + b * bg->hot_k, hot, vals, sums);
+      after_launch(ctx, "k_push_hot");
+      continue;
+    }
+    const unsigned g = grid_for(nt * 32, 256, (int64_t)ctx->num_sms * 8);
     if (wgt)
-      k_push_tiles<true><<<g, kWarps * 32, 0, ctx->stream>>>(
-          bg->col.p, bg->w.p, bg->lro.p + rs + b, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
+      k_push_bits<true><<<g, 256, 0, ctx->stream>>>(
+          bg->col.p, bg->w.p, bg->rstart.p, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
           (uint32_t)Lb, bg->id_map.p + rs, vals, sums);
     else
-      k_push_tiles<false><<<g, kWarps * 32, 0, ctx->stream>>>(
-          bg->col.p, nullptr, bg->lro.p + rs + b, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
+      k_push_bits<false><<<g, 256, 0, ctx->stream>>>(
+          bg->col.p, nullptr, bg->rstart.p, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
           (uint32_t)Lb, bg->id_map.p + rs, vals, sums);
-    after_launch(ctx, "k_push_tiles");
+    after_launch(ctx, "k_push_bits");
   }
 }
 
