@@ -216,7 +216,7 @@ static int carveout_kb() {
   const char *env = getenv("GCB_CARVE_KB");
   return env ? atoi(env) : 132;
 }
-static int64_t hot_capacity(gcb_ctx *ctx) {
+int64_t hot_capacity(gcb_ctx *ctx) {
   int optin = 0;
   GCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   int64_t budget = (int64_t)carveout_kb() * 1024;

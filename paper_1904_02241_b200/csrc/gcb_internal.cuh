@@ -190,7 +190,10 @@ struct gcb_blocked {
   bool is_relabeled = false;         // this object is such a copy
   int64_t fast_iters = 0;            // fast-mode passes run on this graph (tiering)
   gcb_blocked *rl = nullptr;         // the copy (owned), built on first fast call
+  gcb_blocked *hybrid = nullptr;     // degree-ordered copies: push blocking of the edges
+                                     // from cold sources into hot destinations (owned)
   gcb::DArray<uint32_t> rl_perm;     // [n] original id -> renumbered id
+  gcb_blocked *pending_hybrid = nullptr;  // build scratch of ensure_relabeled (owned)
 
   gcb_blocked() = default;
   gcb_blocked(const gcb_blocked &) = delete;
@@ -291,12 +294,14 @@ void cub_sort_pairs_desc_u32_u32(gcb_ctx *ctx, uint32_t *keys, uint32_t *keys_al
                                  uint32_t *vals_alt, int64_t m, uint32_t **res_keys,
                                  uint32_t **res_vals);
 void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sums,
-                  bool use_weights, uint32_t flags, int64_t block_only);
+                  bool use_weights, uint32_t flags, int64_t block_only, bool nonneg = false);
 // relabel.cu: degree-ordered execution copy of a pull graph
 bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters);
 gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg);
 void permute_in(gcb_ctx *ctx, const gcb_blocked *bg, const double *x, double *x_new);
 void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, double *y);
+int64_t hot_capacity(gcb_ctx *ctx);    // gather.cu: pull hot-table slots
+int64_t push_hot_slots(gcb_ctx *ctx);  // pr.cu: push hub-accumulator slots
 // partition.cu: conventional-blocking layout (the CB ablation)
 void to_cb_layout(gcb_ctx *ctx, gcb_blocked *bg);
 void cb_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights, bool exact,

@@ -305,7 +305,11 @@ void compute_range_bounds(gcb_ctx *ctx, const gcb_blocked *bg, int64_t k, int64_
 
 }  // namespace gcb
 
-gcb_blocked::~gcb_blocked() { delete rl; }
+gcb_blocked::~gcb_blocked() {
+  delete rl;
+  delete hybrid;
+  delete pending_hybrid;
+}
 
 namespace gcb {
 

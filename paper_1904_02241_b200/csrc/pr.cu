@@ -522,7 +522,29 @@ __global__ void __launch_bounds__(256)
 // in-degree destinations carries 0x80000000 | slot; those adds go to the
 // CTA's accumulator (shared-memory atomic) and every CTA flushes its
 // non-zero slots with one global RED each at the end.
-template <bool WGT>
+// FIX (non-negative values, i.e. PageRank contributions): the hub table is
+// 64-bit fixed point (2^-62 units) so the shared-memory adds are native
+// integer atomics -- f64 adds on shared memory compile to a CAS loop
+// (ATOMS.CAST.SPIN) that serialises on the hottest hubs.  Sums stay below 1
+// (rank mass), so a CTA's slot cannot overflow; each term is rounded to
+// 2^-62 absolute, and integer adds make the slot order-independent.
+constexpr double kFixScale = 4611686018427387904.0;        // 2^62
+constexpr double kFixInv = 1.0 / 4611686018427387904.0;
+
+// 64-bit shared adds (f64 or u64) are CAS loops on sm_100 (ATOMS.CAST.SPIN);
+// 32-bit ATOMS.ADD is native.  A 64-bit fixed-point slot is therefore two
+// 32-bit words: the low add returns the old word, which tells whether it
+// wrapped, and the carry rides with the high add -- the pair always holds
+// the exact 64-bit sum.
+__device__ __forceinline__ void fix_add(unsigned *lo, unsigned *hi, uint32_t slot,
+                                        unsigned long long add) {
+  const unsigned alo = (unsigned)add, ahi = (unsigned)(add >> 32);
+  const unsigned old = atomicAdd(lo + slot, alo);
+  const unsigned carry = (old + alo < old) ? 1u : 0u;
+  if (ahi + carry) atomicAdd(hi + slot, ahi + carry);
+}
+
+template <bool WGT, bool FIX = false>
 __global__ void __launch_bounds__(1024, 1)
     k_push_hot(const uint32_t *__restrict__ xcol, const double *__restrict__ w,
                const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ tile_row,
@@ -532,10 +554,11 @@ __global__ void __launch_bounds__(1024, 1)
   constexpr int V = kTileV, T = kTileT;
   constexpr uint32_t kHot = 0x80000000u;
   extern __shared__ double s_acc[];
+  unsigned *s_lo = reinterpret_cast<unsigned *>(s_acc), *s_hi = s_lo + hot;
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const uint64_t pol_stream = policy_evict_first();
-  for (int i = threadIdx.x; i < hot; i += blockDim.x) s_acc[i] = 0.0;
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) s_acc[i] = 0.0;  // also 0 in fixed point
   __syncthreads();
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nw) {
@@ -569,13 +592,18 @@ __global__ void __launch_bounds__(1024, 1)
       if (!((tb.vm >> k) & 1u)) continue;
       if (rr >= 32) x = vals[id_map_b[r0 + rr]];
       if (WGT) x = __dmul_rn(ww[k], x);
-      if (c[k] & kHot) atomicAdd(s_acc + (c[k] & ~kHot), x);
-      else atomicAdd(sums + c[k], x);
+      if (c[k] & kHot) {
+        if (FIX) fix_add(s_lo, s_hi, c[k] & ~kHot, __double2ull_rn(x * kFixScale));
+        else atomicAdd(s_acc + (c[k] & ~kHot), x);
+      } else {
+        atomicAdd(sums + c[k], x);
+      }
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < hot; i += blockDim.x) {
-    const double v = s_acc[i];
+    const double v =
+        FIX ? (double)(((unsigned long long)s_hi[i] << 32) | s_lo[i]) * kFixInv : s_acc[i];
     if (v != 0.0) atomicAdd(sums + hot_ids_b[i], v);
   }
 }
@@ -750,7 +778,7 @@ void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out) {
 // ms per iteration: none 3.69, 1K 1.75, 4K 1.48, 16K 1.28, 24K 1.07, 27K 1.07
 // -- REDs need no L1 staging, so unlike the pull gather the table can take
 // most of the shared memory.
-static int64_t push_hot_slots(gcb_ctx *ctx) {
+int64_t push_hot_slots(gcb_ctx *ctx) {
   int optin = 0;
   GCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const char *env = getenv("GCB_PUSH_HOT");
@@ -760,7 +788,7 @@ static int64_t push_hot_slots(gcb_ctx *ctx) {
 }
 
 void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sums, bool use_weights,
-                  uint32_t flags, int64_t block_only) {
+                  uint32_t flags, int64_t block_only, bool nonneg) {
   ensure_derived(ctx, bg);
   if (!(flags & GCB_FLAG_EXACT)) ensure_push_exec(ctx, bg, push_hot_slots(ctx));
   const bool wgt = use_weights && bg->weighted;
@@ -792,10 +820,15 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
       if (smem > done) {
         GCB_CUDA(cudaFuncSetAttribute(k_push_hot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         GCB_CUDA(cudaFuncSetAttribute(k_push_hot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GCB_CUDA(cudaFuncSetAttribute(k_push_hot<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         done = smem;
       }
       const unsigned gh = grid_for(nt * 32, 1024, (int64_t)ctx->num_sms);
-      if (wgt)
+      if (nonneg && !wgt && !getenv("GCB_NO_FIX"))
+        k_push_hot<false, true><<<gh, 1024, smem, ctx->stream>>>(
+            bg->xcol.p, nullptr, bg->rstart.p, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
+            (uint32_t)Lb, bg->id_map.p + rs, bg->hot_ids.p + b * bg->hot_k, hot, vals, sums);
+      else if (wgt)
         k_push_hot<true><<<gh, 1024, smem, ctx->stream>>>(
             bg->xcol.p, bg->w.p, bg->rstart.p, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
             (uint32_t)Lb, bg->id_map.p + rs, bg->hot_ids.p + b * bg->hot_k, hot, vals, sums);
@@ -866,9 +899,16 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   for (int k = 0; k < max_iters; ++k) {
     if (!push) {
       pull_sums(ctx, bg, contrib, contrib32, false, flags, -1, bg->sums.p, true);
+      if (bg->hybrid) {  // relabel.cu: cold-source -> hot-destination edges
+        ProfScope ps(ctx, 0);
+        push_scatter(ctx, bg->hybrid, contrib, bg->sums.p, false, flags, -1, true);
+      }
     } else {
       ProfScope ps(ctx, 0);
-      push_scatter(ctx, bg, bg->contrib.p, bg->sums.p, false, flags, -1);
+      // plain push PageRank keeps the f64 table: measured 1.09 ms vs 1.19 ms per
+      // iteration with the fixed-point one at rmat:24 (its hub slots see far
+      // more adds per CTA than the hybrid's, and the two-word add costs more)
+      push_scatter(ctx, bg, bg->contrib.p, bg->sums.p, false, flags, -1, false);
     }
     {
       ProfScope ps(ctx, 2);
@@ -1047,6 +1087,7 @@ static void pull_spmv(gcb_ctx *ctx, gcb_blocked *bg, const double *x, bool weigh
   }
   GCB_CUDA(cudaMemsetAsync(y, 0, (bg->n ? bg->n : 1) * sizeof(double), ctx->stream));
   pull_sums(ctx, bg, x, nullptr, weights, flags, -1, y, true);
+  if (bg->hybrid) push_scatter(ctx, bg->hybrid, x, y, weights, flags, -1);
 }
 
 int gcb_segment_row_sums(gcb_ctx *ctx, const gcb_csr *g, const double *values_host, int use_weights,

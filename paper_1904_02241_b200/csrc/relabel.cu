@@ -16,6 +16,7 @@
 // reassociation (the fast-mode contract, <= 1e-6 relative); the exact mode
 // never uses this layout.
 #include <cstdlib>
+#include <utility>
 
 #include "gcb_internal.cuh"
 
@@ -73,6 +74,119 @@ __global__ void k_permute_out(int64_t n, const uint32_t *__restrict__ perm,
 // that stays resident.  A graph is promoted once it has run
 // GCB_RELABEL_AFTER fast-mode iterations (default 20; 0 = immediately); a
 // graph uploaded for one short call never is.
+// ---------------------------------------------------------------------------
+// Hybrid split of the degree-ordered copy.  Every cold gather of the pull
+// kernel costs one L1->XBAR request (gather.cu), but an edge from a cold
+// source into a hub destination need not: in push form its source value is
+// read once per source row (sequential ids) and the add lands in the
+// shared-memory hub table of k_push_hot.  So edges (u -> v) with u outside its
+// block's hot prefix and v among the top-H destinations by in-degree move to
+// a push blocking that runs after the pull pass (rmat:24: A hot-source 29.9%,
+// B cold-source/hub-destination 24.0%, C both cold 46.1% of the edges).
+// ---------------------------------------------------------------------------
+bool hybrid_enabled() {
+  const char *env = getenv("GCB_HYBRID");
+  return !(env && env[0] == '0');
+}
+
+__global__ void k_count_u32(int64_t m, const uint32_t *__restrict__ ids, uint32_t *__restrict__ cnt) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + ids[e], 1u);
+}
+
+__global__ void k_mark_top(int64_t K, const uint32_t *__restrict__ keys, const uint32_t *__restrict__ ids,
+                           uint8_t *__restrict__ hot) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (keys[i] > 0) hot[ids[i]] = 1;
+}
+
+__global__ void k_class_b(int64_t m, const uint32_t *__restrict__ rows, const uint32_t *__restrict__ cols,
+                          int64_t width, uint32_t hs, const uint8_t *__restrict__ hot_dst,
+                          uint32_t *__restrict__ flag) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = cols[e];
+    const bool cold_src = (uint32_t)((int64_t)u % width) >= hs;
+    flag[e] = (cold_src && hot_dst[rows[e]]) ? 1u : 0u;
+  }
+}
+
+// stable split: flag 1 -> (a_*) at pos[e], flag 0 -> (b_*) at e - pos[e]
+__global__ void k_split_edges(int64_t m, const uint32_t *__restrict__ flag, const uint32_t *__restrict__ pos,
+                              const uint32_t *__restrict__ rows, const uint32_t *__restrict__ cols,
+                              const double *__restrict__ w, uint32_t *__restrict__ a_src,
+                              uint32_t *__restrict__ a_dst, double *__restrict__ a_w,
+                              uint32_t *__restrict__ b_rows, uint32_t *__restrict__ b_cols,
+                              double *__restrict__ b_w) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = pos[e];
+    if (flag[e]) {
+      a_src[p] = cols[e];  // push form: rows = sources
+      a_dst[p] = rows[e];
+      if (w) a_w[p] = w[e];
+    } else {
+      const int64_t q = e - p;
+      b_rows[q] = rows[e];
+      b_cols[q] = cols[e];
+      if (w) b_w[q] = w[e];
+    }
+  }
+}
+
+// rows/cols (renumbered transpose edges, in place) keep the pull edges;
+// returns their count and the push CSR of the split-off edges
+int64_t hybrid_split(gcb_ctx *ctx, gcb_blocked *bg, DArray<uint32_t> &rows, DArray<uint32_t> &cols,
+                     const double *w, DArray<double> &w_pull, gcb_csr **push_csr) {
+  const int64_t n = bg->n, m = bg->m;
+  *push_csr = nullptr;
+  const int64_t hs = hot_capacity(ctx);
+  const int64_t hd = push_hot_slots(ctx);
+  if (hs <= 0 || hd <= 0 || bg->width <= hs) return m;  // whole slices are hot already
+  DArray<uint8_t> hot_dst(n);
+  {
+    DArray<uint32_t> k1(n), k2(n), v1(n), v2(n);
+    GCB_CUDA(cudaMemsetAsync(k1.p, 0, n * sizeof(uint32_t), ctx->stream));
+    k_count_u32<<<grid_for(m, 256, 65536), 256, 0, ctx->stream>>>(m, rows.p, k1.p);
+    after_launch(ctx, "k_count_u32");
+    k_iota_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, v1.p);
+    after_launch(ctx, "k_iota_u32");
+    uint32_t *rk = nullptr, *rv = nullptr;
+    cub_sort_pairs_desc_u32_u32(ctx, k1.p, k2.p, v1.p, v2.p, n, &rk, &rv);
+    GCB_CUDA(cudaMemsetAsync(hot_dst.p, 0, n, ctx->stream));
+    const int64_t K = hd < n ? hd : n;
+    k_mark_top<<<grid_for(K, 256, 4096), 256, 0, ctx->stream>>>(K, rk, rv, hot_dst.p);
+    after_launch(ctx, "k_mark_top");
+  }
+  DArray<uint32_t> flag(m + 1), pos(m + 1);
+  k_class_b<<<grid_for(m, 256, 65536), 256, 0, ctx->stream>>>(m, rows.p, cols.p, bg->width,
+                                                             (uint32_t)hs, hot_dst.p, flag.p);
+  after_launch(ctx, "k_class_b");
+  GCB_CUDA(cudaMemsetAsync(flag.p + m, 0, sizeof(uint32_t), ctx->stream));
+  cub_exclusive_sum_u32(ctx, flag.p, pos.p, m + 1);
+  uint32_t mb = 0;
+  d2h(ctx, &mb, pos.p + m, 1);
+  sync(ctx);
+  if (mb == 0) return m;
+  const int64_t mp = m - mb;
+  DArray<uint32_t> a_src(mb), a_dst(mb), b_rows(mp ? mp : 1), b_cols(mp ? mp : 1);
+  DArray<double> a_w;
+  if (w) {
+    a_w.alloc(mb);
+    w_pull.alloc(mp ? mp : 1);
+  }
+  k_split_edges<<<grid_for(m, 256, 65536), 256, 0, ctx->stream>>>(
+      m, flag.p, pos.p, rows.p, cols.p, w, a_src.p, a_dst.p, w ? a_w.p : nullptr, b_rows.p,
+      b_cols.p, w ? w_pull.p : nullptr);
+  after_launch(ctx, "k_split_edges");
+  *push_csr = csr_from_device_edges(ctx, n, mb, a_src.p, a_dst.p, w ? a_w.p : nullptr);
+  rows = std::move(b_rows);
+  cols = std::move(b_cols);
+  return mp;
+}
+
 bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters) {
   if (flags & (GCB_FLAG_EXACT | GCB_FLAG_NO_RELABEL)) return false;
   if (bg->direction != 0 || bg->m == 0 || bg->n >= (int64_t(1) << 32)) return false;
@@ -117,18 +231,55 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
           cols.p + es);
       after_launch(ctx, "k_relabel_block");
     }
-    // 3. canonical CSR of the renumbered transpose, then the same TOCAB cut
-    csr = csr_from_device_edges(ctx, n, m, rows.p, cols.p, bg->weighted ? bg->w.p : nullptr);
+    // 3. split off the edges whose source misses its block's hot prefix but
+    //    whose destination is a hub (hybrid_split), then the canonical CSR of
+    //    the rest of the renumbered transpose and the same TOCAB cut
+    gcb_csr *push_csr = nullptr;
+    int64_t m_pull = m;
+    const double *w = bg->weighted ? bg->w.p : nullptr;
+    DArray<double> wpull;
+    if (hybrid_enabled()) {
+      m_pull = hybrid_split(ctx, bg, rows, cols, w, wpull, &push_csr);
+      if (push_csr && bg->weighted) w = wpull.p;  // split: the pull edges' own weights
+    }
+    try {
+      csr = csr_from_device_edges(ctx, n, m_pull, rows.p, cols.p, w);
+    } catch (...) {
+      if (push_csr) gcb_csr_destroy(push_csr);
+      throw;
+    }
+    if (push_csr) {
+      try {
+        bg->pending_hybrid = partition_device(ctx, push_csr, 1, n);  // one block: every hub slot
+      } catch (...) {
+        gcb_csr_destroy(push_csr);
+        gcb_csr_destroy(csr);
+        throw;
+      }
+      gcb_csr_destroy(push_csr);
+    }
   }
   try {
     gcb_blocked *rl = partition_device(ctx, csr, 0, bg->width);
     rl->is_relabeled = true;
+    if (bg->pending_hybrid) {
+      rl->hybrid = bg->pending_hybrid;
+      bg->pending_hybrid = nullptr;
+      // the pull copy no longer holds every edge: its out-degrees are the
+      // whole graph's, renumbered (kernels.py:324-330)
+      rl->deg.alloc(n);
+      k_permute_in<uint32_t><<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(
+          n, bg->rl_perm.p, bg->deg.p, rl->deg.p);
+      after_launch(ctx, "k_permute_in");
+      rl->deg_ready = true;
+    }
     bg->rl = rl;
   } catch (...) {
     gcb_csr_destroy(csr);
     throw;
   }
   gcb_csr_destroy(csr);
+  sync(ctx);
   return bg->rl;
 }
 
