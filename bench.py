@@ -342,7 +342,8 @@ def run_ours(args):
         except Exception:
             traffic = None
     roofline = {
-        "bound": "hbm", "kernel": "k_pull_hot (TOCAB pull gather, gather.cu)",
+        "bound": "hbm",
+        "kernel": "k_pull_hot (TOCAB pull gather) + k_push_hot (hybrid hub-destination edges)",
         "achieved": round(g_achieved, 1) if g_achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(g_achieved / peak, 4) if g_achieved else None,
         "traffic": traffic, "peak_source": peak_kind,
