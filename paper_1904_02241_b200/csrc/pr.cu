@@ -440,8 +440,9 @@ __global__ void __launch_bounds__(512, 2)
 }
 
 static unsigned update_grid(gcb_ctx *ctx, int64_t n) {
-  static int per_sm = getenv("GCB_UPD_CTAS") ? atoi(getenv("GCB_UPD_CTAS")) : 1 << 20;
-  return grid_for((n + 3) / 4, 512, (int64_t)per_sm * ctx->num_sms);
+  // one 4-vertex quad per thread: 111 us at rmat:24 against 125 us with two
+  // persistent CTAs per SM (scripts/mb_stream.cu)
+  return grid_for((n + 3) / 4, 512, (int64_t)(1 << 20) * ctx->num_sms);
 }
 
 static void launch_update(gcb_ctx *ctx, bool exact, int64_t n, double base, double damping,
@@ -701,7 +702,7 @@ void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *v
     cb_sums(ctx, bg, vals, use_weights, exact, out);  // partition.cu: the CB ablation
     return;
   }
-  if (accum && !exact && vals && !vals32 && block_only < 0 && getenv("GCB_OLD_GATHER") == nullptr) {
+  if (accum && !exact && vals && !vals32 && block_only < 0) {
     gather_accum(ctx, bg, vals, use_weights, flags, out);  // gather.cu: hot-staged path
     return;
   }
