@@ -48,47 +48,6 @@ __global__ void k_bfs_pull_block(int64_t Lb, const uint32_t *__restrict__ lro_b,
   }
 }
 
-// commit level: flags -> ascending queue slice, depth stamp, new bitmap, and
-// the frontier's total out-degree (choose_direction traversal.py:93-99)
-__global__ void k_bfs_commit(int64_t n, int32_t level, uint8_t *__restrict__ next,
-                             const uint32_t *__restrict__ pos, uint32_t *__restrict__ queue_out,
-                             int32_t *__restrict__ depth, uint32_t *__restrict__ front_bits,
-                             const int64_t *__restrict__ ro,
-                             unsigned long long *__restrict__ deg_sum) {
-  __shared__ unsigned long long s_sum;
-  if (threadIdx.x == 0) s_sum = 0;
-  __syncthreads();
-  unsigned long long local = 0;
-  const int64_t nwords = (n + 31) >> 5;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nwords * 32;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = base + threadIdx.x;
-    bool f = false;
-    if (v < n) {
-      f = next[v] != 0;
-      if (f) {
-        queue_out[pos[v]] = (uint32_t)v;
-        depth[v] = level;
-        next[v] = 0;
-        local += (unsigned long long)(ro[v + 1] - ro[v]);
-      }
-    }
-    const unsigned word = __ballot_sync(0xffffffffu, f);
-    if ((threadIdx.x & 31) == 0 && (v >> 5) < nwords) front_bits[v >> 5] = word;
-  }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xffffffffu, local, d);
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_sum, local);
-  __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(deg_sum, s_sum);
-}
-
-__global__ void k_flags_u32(int64_t n, const uint8_t *__restrict__ next, uint32_t *__restrict__ f) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x)
-    f[v] = next[v];
-}
-
 static gcb_blocked *default_pull_blocking(gcb_ctx *ctx, const gcb_csr *g,
                                           gcb_blocked **owned) {
   // traversal.py:186-187: partition_tocab(transpose(g), "pull", max(1, n // 8))
@@ -105,13 +64,17 @@ static gcb_blocked *default_pull_blocking(gcb_ctx *ctx, const gcb_csr *g,
   return *owned;
 }
 
+// Level commit (compact_commit below): a CTA of 256 threads x 16 vertices
+// (one 16-byte vector of next-frontier flags each) covers 4096 vertices.
+constexpr int kCmpT = 256, kCmpV = 16, kCmpChunk = kCmpT * kCmpV;
+
 struct Frontier {
-  DArray<uint8_t> next;
+  DArray<uint8_t> next;  // padded to a multiple of kCmpChunk; the pad stays 0
   DArray<uint32_t> flags, pos, bits;
   DArray<uint32_t> qdeg, qoff;  // edge-balanced push: queue degrees and their prefix
   DArray<unsigned long long> degsum;
   explicit Frontier(int64_t n) {
-    next.alloc(n ? n : 1);
+    next.alloc((size_t)ceil_div(n > 0 ? n : 1, kCmpChunk) * kCmpChunk);
     flags.alloc(n + 1);
     pos.alloc(n + 1);
     bits.alloc((n + 31) / 32 + 1);
@@ -120,6 +83,126 @@ struct Frontier {
     degsum.alloc(1);
   }
 };
+
+// What a committed vertex v gets besides its queue slot (null = skip).
+struct CommitOps {
+  int32_t level = 0;
+  int32_t *depth = nullptr;  // depth[v] = level
+  double *sigma = nullptr;   // sigma[v] += sig_add[v]; sig_add[v] = 0
+  double *sig_add = nullptr;
+  uint32_t *bits = nullptr;  // bitmap of the committed level (every word rewritten)
+  const int64_t *ro = nullptr;
+  unsigned long long *degsum = nullptr;  // += out-degree of every committed vertex
+};
+
+// bit k = flag byte k of the 16 is nonzero
+__device__ __forceinline__ uint32_t flag_mask16(uint4 w) {
+  const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+  uint32_t m = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if ((x[j] >> (8 * b)) & 0xffu) m |= 1u << (4 * j + b);
+  return m;
+}
+
+__global__ void __launch_bounds__(kCmpT) k_cmp_count(const uint8_t *__restrict__ next,
+                                                     uint32_t *__restrict__ cnt) {
+  __shared__ uint32_t s_w[kCmpT / 32];
+  const int64_t v0 = (int64_t)blockIdx.x * kCmpChunk + threadIdx.x * kCmpV;
+  const uint32_t c = __reduce_add_sync(0xffffffffu,
+                                       (unsigned)__popc(flag_mask16(*reinterpret_cast<const uint4 *>(next + v0))));
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int i = 0; i < kCmpT / 32; ++i) t += s_w[i];
+    cnt[blockIdx.x] = t;
+  }
+}
+
+// queue[off[cta] + rank of v among the CTA's flagged vertices] = v, in vertex
+// order; clears the flags and applies op
+__global__ void __launch_bounds__(kCmpT) k_cmp_commit(int64_t n, uint8_t *__restrict__ next,
+                                                      const uint32_t *__restrict__ off,
+                                                      uint32_t *__restrict__ queue, CommitOps op) {
+  __shared__ uint32_t s_w[kCmpT / 32];
+  __shared__ unsigned long long s_sum;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t v0 = (int64_t)blockIdx.x * kCmpChunk + threadIdx.x * kCmpV;
+  uint4 *np = reinterpret_cast<uint4 *>(next + v0);
+  const uint32_t m = flag_mask16(*np);
+  const uint32_t c = __popc(m);
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  if (threadIdx.x == 0) s_sum = 0;
+  __syncthreads();
+  uint32_t pos = off[blockIdx.x] + incl - c;
+  for (int i = 0; i < warp; ++i) pos += s_w[i];
+  unsigned long long local = 0;
+  if (m) {
+    *np = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 1
+    for (uint32_t mm = m; mm; mm &= mm - 1) {
+      const int64_t v = v0 + __ffs(mm) - 1;
+      queue[pos++] = (uint32_t)v;
+      if (op.depth) op.depth[v] = op.level;
+      if (op.sigma) {
+        op.sigma[v] = __dadd_rn(op.sigma[v], op.sig_add[v]);
+        op.sig_add[v] = 0.0;
+      }
+      if (op.degsum) local += (unsigned long long)(op.ro[v + 1] - op.ro[v]);
+    }
+  }
+  if (op.bits) {
+    const uint32_t hi = __shfl_down_sync(FULL, m, 1);
+    if (!(lane & 1) && v0 < n) op.bits[v0 >> 5] = m | (hi << 16);
+  }
+  if (op.degsum) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(FULL, local, d);
+    if (lane == 0 && local) atomicAdd(&s_sum, local);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_sum) atomicAdd(op.degsum, s_sum);
+  }
+}
+
+// Commit the flagged next frontier: count per CTA, scan the CTA counts, write
+// (replaces flags -> u32 copy -> n-element scan -> commit: 135-175 us per
+// level at rmat:24).  Returns the committed count and, with want_degsum, the
+// committed vertices' out-degree sum.
+static int64_t compact_commit(gcb_ctx *ctx, Frontier &F, int64_t n, CommitOps op, uint32_t *queue,
+                              bool want_degsum, uint64_t *degsum) {
+  const int64_t nb = ceil_div(n, kCmpChunk);
+  if (nb == 0) return 0;
+  k_cmp_count<<<(unsigned)nb, kCmpT, 0, ctx->stream>>>(F.next.p, F.flags.p);
+  after_launch(ctx, "k_cmp_count");
+  GCB_CUDA(cudaMemsetAsync(F.flags.p + nb, 0, sizeof(uint32_t), ctx->stream));
+  cub_exclusive_sum_u32(ctx, F.flags.p, F.pos.p, nb + 1);
+  if (want_degsum) {
+    GCB_CUDA(cudaMemsetAsync(F.degsum.p, 0, sizeof(unsigned long long), ctx->stream));
+    op.degsum = F.degsum.p;
+  } else {
+    op.degsum = nullptr;
+  }
+  k_cmp_commit<<<(unsigned)nb, kCmpT, 0, ctx->stream>>>(n, F.next.p, F.pos.p, queue, op);
+  after_launch(ctx, "k_cmp_commit");
+  uint32_t *h = (uint32_t *)ctx->pinned;
+  unsigned long long *hs = (unsigned long long *)((char *)ctx->pinned + 64);
+  d2h(ctx, h, F.pos.p + nb, 1);
+  if (want_degsum) d2h(ctx, hs, F.degsum.p, 1);
+  sync(ctx);
+  if (degsum) *degsum = want_degsum ? *hs : 0;
+  return (int64_t)*h;
+}
 
 // Edge-balanced push (a frontier holding one hub -- vertex 0 of rmat:24 has
 // 370K out-edges -- left a warp-per-vertex push on one warp for 3.4 ms):
@@ -168,23 +251,12 @@ __global__ void k_bfs_push_eb(int64_t total, int64_t qsize, const uint32_t *__re
 // flags -> queue slice at `out`; returns (count, degree sum) after a sync
 static void commit_level(gcb_ctx *ctx, const gcb_csr *g, Frontier &F, int32_t level,
                          uint32_t *out, int32_t *depth, int64_t *count, uint64_t *degsum) {
-  const int64_t n = g->n;
-  k_flags_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, F.next.p, F.flags.p);
-  after_launch(ctx, "k_flags_u32");
-  GCB_CUDA(cudaMemsetAsync(F.flags.p + n, 0, sizeof(uint32_t), ctx->stream));
-  cub_exclusive_sum_u32(ctx, F.flags.p, F.pos.p, n + 1);
-  GCB_CUDA(cudaMemsetAsync(F.degsum.p, 0, sizeof(unsigned long long), ctx->stream));
-  k_bfs_commit<<<grid_for(((n + 31) / 32) * 32, 256, (int64_t)ctx->num_sms * 8), 256, 0,
-                 ctx->stream>>>(n, level, F.next.p, F.pos.p, out, depth, F.bits.p, g->ro.p,
-                                F.degsum.p);
-  after_launch(ctx, "k_bfs_commit");
-  uint32_t *h = (uint32_t *)ctx->pinned;
-  unsigned long long *hs = (unsigned long long *)((char *)ctx->pinned + 64);
-  d2h(ctx, h, F.pos.p + n, 1);
-  d2h(ctx, hs, F.degsum.p, 1);
-  sync(ctx);
-  *count = *h;
-  *degsum = *hs;
+  CommitOps op;
+  op.level = level;
+  op.depth = depth;
+  op.bits = F.bits.p;
+  op.ro = g->ro.p;
+  *count = compact_commit(ctx, F, g->n, op, out, true, degsum);
 }
 
 __global__ void k_fill_i32(int64_t n, int32_t v, int32_t *p) {
@@ -212,7 +284,7 @@ static void bfs_run(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int64_t sou
   Frontier F(n);
   k_fill_i32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, kInfDepth, depth_dev);
   after_launch(ctx, "k_fill_i32");
-  GCB_CUDA(cudaMemsetAsync(F.next.p, 0, n, ctx->stream));
+  GCB_CUDA(cudaMemsetAsync(F.next.p, 0, F.next.n, ctx->stream));
   GCB_CUDA(cudaMemsetAsync(F.bits.p, 0, ((n + 31) / 32 + 1) * sizeof(uint32_t), ctx->stream));
   k_seed<<<1, 1, 0, ctx->stream>>>(source, depth_dev, levels_dev, F.bits.p);
   after_launch(ctx, "k_seed");
@@ -335,38 +407,6 @@ __global__ void __launch_bounds__(256)
           }
         });
   }
-}
-
-// commit round: flags -> queue, bitmap; returns count + frontier out-degree
-__global__ void k_sssp_commit(int64_t n, uint8_t *__restrict__ next, const uint32_t *__restrict__ pos,
-                              uint32_t *__restrict__ queue_out, uint32_t *__restrict__ front_bits,
-                              const int64_t *__restrict__ ro,
-                              unsigned long long *__restrict__ deg_sum) {
-  __shared__ unsigned long long s_sum;
-  if (threadIdx.x == 0) s_sum = 0;
-  __syncthreads();
-  unsigned long long local = 0;
-  const int64_t nwords = (n + 31) >> 5;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nwords * 32;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = base + threadIdx.x;
-    bool f = false;
-    if (v < n) {
-      f = next[v] != 0;
-      if (f) {
-        queue_out[pos[v]] = (uint32_t)v;
-        next[v] = 0;
-        local += (unsigned long long)(ro[v + 1] - ro[v]);
-      }
-    }
-    const unsigned word = __ballot_sync(0xffffffffu, f);
-    if ((threadIdx.x & 31) == 0 && (v >> 5) < nwords) front_bits[v >> 5] = word;
-  }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xffffffffu, local, d);
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_sum, local);
-  __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(deg_sum, s_sum);
 }
 
 // --------------------------------------------------------------------------
@@ -533,7 +573,7 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
   Frontier F(n);
   k_fill_i64<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, kInfDist, dist.p);
   after_launch(ctx, "k_fill_i64");
-  GCB_CUDA(cudaMemsetAsync(F.next.p, 0, n, ctx->stream));
+  GCB_CUDA(cudaMemsetAsync(F.next.p, 0, F.next.n, ctx->stream));
   GCB_CUDA(cudaMemsetAsync(F.bits.p, 0, ((n + 31) / 32 + 1) * sizeof(uint32_t), ctx->stream));
   {
     int64_t zero = 0;
@@ -579,21 +619,12 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
       }
     }
     // compact next flags into the queue
-    k_flags_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, F.next.p, F.flags.p);
-    after_launch(ctx, "k_flags_u32");
-    GCB_CUDA(cudaMemsetAsync(F.flags.p + n, 0, sizeof(uint32_t), ctx->stream));
-    cub_exclusive_sum_u32(ctx, F.flags.p, F.pos.p, n + 1);
-    GCB_CUDA(cudaMemsetAsync(F.degsum.p, 0, sizeof(unsigned long long), ctx->stream));
-    k_sssp_commit<<<grid_for(((n + 31) / 32) * 32, 256, (int64_t)ctx->num_sms * 8), 256, 0,
-                    ctx->stream>>>(n, F.next.p, F.pos.p, queue.p, F.bits.p, g->ro.p, F.degsum.p);
-    after_launch(ctx, "k_sssp_commit");
-    uint32_t *h = (uint32_t *)ctx->pinned;
-    unsigned long long *hs = (unsigned long long *)((char *)ctx->pinned + 64);
-    d2h(ctx, h, F.pos.p + n, 1);
-    d2h(ctx, hs, F.degsum.p, 1);
-    sync(ctx);
-    qsize = *h;
-    work = *hs;
+    CommitOps op;
+    op.bits = F.bits.p;
+    op.ro = g->ro.p;
+    uint64_t ds = 0;
+    qsize = compact_commit(ctx, F, n, op, queue.p, true, &ds);
+    work = ds;
     ++r;
   }
   d2h(ctx, dist_host, dist.p, n);
@@ -695,23 +726,6 @@ __global__ void k_step_pull(int64_t Lb, const uint32_t *__restrict__ lro_b,
   }
 }
 
-__global__ void k_step_commit(int64_t n, int32_t level, uint8_t *__restrict__ next,
-                              const uint32_t *__restrict__ pos, uint32_t *__restrict__ queue_out,
-                              int32_t *__restrict__ depth, double *__restrict__ sigma,
-                              double *__restrict__ sig_add) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    if (!next[v]) continue;
-    queue_out[pos[v]] = (uint32_t)v;
-    depth[v] = level;
-    next[v] = 0;
-    if (sigma) {
-      sigma[v] += sig_add[v];
-      sig_add[v] = 0.0;
-    }
-  }
-}
-
 __global__ void k_set_bits(int64_t q, const uint32_t *__restrict__ queue, uint32_t *__restrict__ bits) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -736,7 +750,7 @@ extern "C" int gcb_bfs_step(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull
   Frontier F(n);
   h2d(ctx, depth.p, depth_host, n);
   h2d(ctx, queue.p, frontier_host, frontier_size);
-  GCB_CUDA(cudaMemsetAsync(F.next.p, 0, n ? n : 1, ctx->stream));
+  GCB_CUDA(cudaMemsetAsync(F.next.p, 0, F.next.n, ctx->stream));
   if (sigma_host_or_null) {
     sigma.alloc(n ? n : 1);
     sig_add.alloc(n ? n : 1);
@@ -776,16 +790,12 @@ extern "C" int gcb_bfs_step(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull
       after_launch(ctx, "k_step_pull");
     }
   }
-  k_flags_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, F.next.p, F.flags.p);
-  after_launch(ctx, "k_flags_u32");
-  GCB_CUDA(cudaMemsetAsync(F.flags.p + n, 0, sizeof(uint32_t), ctx->stream));
-  cub_exclusive_sum_u32(ctx, F.flags.p, F.pos.p, n + 1);
-  k_step_commit<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, level + 1, F.next.p, F.pos.p,
-                                                                  out.p, depth.p, sg, sig_add.p);
-  after_launch(ctx, "k_step_commit");
-  uint32_t cnt = 0;
-  d2h(ctx, &cnt, F.pos.p + n, 1);
-  sync(ctx);
+  CommitOps op;
+  op.level = level + 1;
+  op.depth = depth.p;
+  op.sigma = sg;
+  op.sig_add = sg ? sig_add.p : nullptr;
+  const int64_t cnt = compact_commit(ctx, F, n, op, out.p, false, nullptr);
   *next_size = cnt;
   d2h(ctx, depth_host, depth.p, n);
   if (sigma_host_or_null) d2h(ctx, sigma_host_or_null, sigma.p, n);
@@ -903,43 +913,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// commit a level with path counts: ascending queue slice, depth stamp,
-// sigma += sig_add, the next frontier bitmap and its out-degree sum
-__global__ void k_bc_commit(int64_t n, int32_t level, uint8_t *__restrict__ next,
-                            const uint32_t *__restrict__ pos, uint32_t *__restrict__ queue_out,
-                            int32_t *__restrict__ depth, double *__restrict__ sigma,
-                            double *__restrict__ sig_add, uint32_t *__restrict__ front_bits,
-                            const int64_t *__restrict__ ro, unsigned long long *__restrict__ deg_sum) {
-  __shared__ unsigned long long s_sum;
-  if (threadIdx.x == 0) s_sum = 0;
-  __syncthreads();
-  unsigned long long local = 0;
-  const int64_t nwords = (n + 31) >> 5;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nwords * 32;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = base + threadIdx.x;
-    bool f = false;
-    if (v < n) {
-      f = next[v] != 0;
-      if (f) {
-        queue_out[pos[v]] = (uint32_t)v;
-        depth[v] = level;
-        next[v] = 0;
-        sigma[v] = __dadd_rn(sigma[v], sig_add[v]);
-        sig_add[v] = 0.0;
-        local += (unsigned long long)(ro[v + 1] - ro[v]);
-      }
-    }
-    const unsigned word = __ballot_sync(0xffffffffu, f);
-    if ((threadIdx.x & 31) == 0 && (v >> 5) < nwords) front_bits[v >> 5] = word;
-  }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) local += __shfl_down_sync(0xffffffffu, local, d);
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_sum, local);
-  __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(deg_sum, s_sum);
-}
-
 __global__ void k_bc_seed(int64_t src, int32_t *depth, double *sigma, uint32_t *queue,
                           uint32_t *bits) {
   depth[src] = 0;
@@ -1017,23 +990,18 @@ static void bc_forward_dev(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int6
         after_launch(ctx, "k_bc_pull_tiles");
       }
     }
-    k_flags_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, F.next.p, F.flags.p);
-    after_launch(ctx, "k_flags_u32");
-    GCB_CUDA(cudaMemsetAsync(F.flags.p + n, 0, sizeof(uint32_t), ctx->stream));
-    cub_exclusive_sum_u32(ctx, F.flags.p, F.pos.p, n + 1);
-    GCB_CUDA(cudaMemsetAsync(F.degsum.p, 0, sizeof(unsigned long long), ctx->stream));
-    k_bc_commit<<<grid_for(((n + 31) / 32) * 32, 256, (int64_t)ctx->num_sms * 8), 256, 0,
-                  ctx->stream>>>(n, level + 1, F.next.p, F.pos.p, levels + qoff + qsize, depth,
-                                 sigma, sig_add, F.bits.p, g->ro.p, F.degsum.p);
-    after_launch(ctx, "k_bc_commit");
-    uint32_t *h = (uint32_t *)ctx->pinned;
-    unsigned long long *hs = (unsigned long long *)((char *)ctx->pinned + 64);
-    d2h(ctx, h, F.pos.p + n, 1);
-    d2h(ctx, hs, F.degsum.p, 1);
-    sync(ctx);
+    CommitOps op;
+    op.level = level + 1;
+    op.depth = depth;
+    op.sigma = sigma;
+    op.sig_add = sig_add;
+    op.bits = F.bits.p;
+    op.ro = g->ro.p;
+    uint64_t ds = 0;
+    const int64_t cnt = compact_commit(ctx, F, n, op, levels + qoff + qsize, true, &ds);
     qoff += qsize;
-    qsize = *h;
-    work = *hs;
+    qsize = cnt;
+    work = ds;
     ++level;
     if (qsize) off.push_back(qoff + qsize);
   }
@@ -1092,7 +1060,7 @@ extern "C" int gcb_bc(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, cons
     DArray<double> sigma(n ? n : 1), sig_add(n ? n : 1), delta(n ? n : 1), cent(n ? n : 1);
     DArray<uint32_t> levels(n ? n : 1);
     Frontier F(n);
-    GCB_CUDA(cudaMemsetAsync(F.next.p, 0, n ? n : 1, ctx->stream));
+    GCB_CUDA(cudaMemsetAsync(F.next.p, 0, F.next.n, ctx->stream));
     GCB_CUDA(cudaMemsetAsync(sig_add.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));
     GCB_CUDA(cudaMemsetAsync(delta.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));
     GCB_CUDA(cudaMemsetAsync(cent.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));

@@ -174,7 +174,8 @@ def bfs(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
         _lib.ptr(verts, _lib.P_u32), _lib.ptr(sizes, _lib.P_i64), _lib.ptr(dirs, _lib.P_u8), cap,
         ctypes.byref(nl), ctypes.byref(ne)), "bfs")
     bounds = np.concatenate([[0], np.cumsum(sizes[: nl.value])])
-    levels = [verts[bounds[i]:bounds[i + 1]].copy() for i in range(nl.value)]
+    # views into the one pinned queue array (a per-level copy cost 3-7 ms at rmat:24)
+    levels = [verts[bounds[i]:bounds[i + 1]] for i in range(nl.value)]
     directions = ["blocked-pull" if d else "push" for d in dirs[: ne.value]]
     return BfsResult(depth, levels, directions)
 
