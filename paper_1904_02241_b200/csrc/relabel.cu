@@ -84,10 +84,20 @@ __global__ void k_permute_out(int64_t n, const uint32_t *__restrict__ perm,
 // a push blocking that runs after the pull pass (rmat:24: A hot-source 29.9%,
 // B cold-source/hub-destination 24.0%, C both cold 46.1% of the edges).
 // ---------------------------------------------------------------------------
-bool hybrid_enabled() {
+// GCB_HYBRID: 0 off, 1 (default) when the cost model below says it pays, 2 always
+static int hybrid_mode() {
   const char *env = getenv("GCB_HYBRID");
-  return !(env && env[0] == '0');
+  return env && env[0] ? atoi(env) : 1;
 }
+
+bool hybrid_enabled() { return hybrid_mode() != 0; }
+
+// The push pass has a fixed cost -- its own launch, and every CTA flushes its
+// hub table (num_sms x slots global adds) -- against a per-edge saving over the
+// pull gather.  Fitted on rmat:21/22/24/25:44 (ms per iteration, hybrid minus
+// pull-only: +0.032, +0.024, -0.015, -0.26 for 9.7M/19M/64M/370M hub edges):
+// +40 us fixed, -0.85 ps per edge moved, break-even near 13 x num_sms x slots.
+constexpr int64_t kHybridMinEdgesPerSlot = 14;
 
 __global__ void k_count_u32(int64_t m, const uint32_t *__restrict__ ids, uint32_t *__restrict__ cnt) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
@@ -170,6 +180,7 @@ int64_t hybrid_split(gcb_ctx *ctx, gcb_blocked *bg, DArray<uint32_t> &rows, DArr
   d2h(ctx, &mb, pos.p + m, 1);
   sync(ctx);
   if (mb == 0) return m;
+  if (hybrid_mode() == 1 && (int64_t)mb < kHybridMinEdgesPerSlot * ctx->num_sms * hd) return m;
   const int64_t mp = m - mb;
   DArray<uint32_t> a_src(mb), a_dst(mb), b_rows(mp ? mp : 1), b_cols(mp ? mp : 1);
   DArray<double> a_w;
