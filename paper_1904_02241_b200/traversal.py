@@ -260,19 +260,24 @@ def bc(g: CsrGraph, sources, g_blocked: BlockedGraph | None = None,
 
 
 def sssp(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
-         policy: DirectionPolicy = DirectionPolicy(value_bytes=8)) -> SsspResult:
+         policy: DirectionPolicy | None = None) -> SsspResult:
     """Single-source shortest paths over non-negative integer edge weights.
 
     Not in the reference (SPEC.md:381 lists SSSP as a non-goal); named by the
     north star.  ``g`` must carry integral float64 weights (< 2^53).  Frontier
     Bellman-Ford; each round pushes (64-bit atomicMin) or pulls over the TOCAB
     blocks of the weighted transpose by choose_direction's rule.  Parallel
-    edges act as their minimum weight."""
+    edges act as their minimum weight.  The default policy takes the device's
+    own L2 as the cache capacity (8-byte distances): a pull round scans every
+    in-edge, so it pays only once the frontier's edges overflow the L2
+    (rmat:24 from 0: 14.4 ms with the 1080 Ti's 2.75 MB, 10.9 ms with 126 MB)."""
     _check_source(g, source)
     if not g.weighted:
         raise ValueError("sssp needs integer edge weights on the graph")
     n = g.num_vertices
     h = g.device()
+    if policy is None:
+        policy = DirectionPolicy(cache_capacity_bytes=int(h.ctx.info()["l2_bytes"]), value_bytes=8)
     bgh = None
     if policy.mode != "force-push":
         if g_blocked is None:
