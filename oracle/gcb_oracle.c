@@ -174,7 +174,7 @@ int orc_transpose(int64_t n, int64_t m, const int64_t *ro, const uint32_t *col,
  * ------------------------------------------------------------------------- */
 int orc_partition_sizes(int64_t n, int64_t m, const int64_t *ro, const uint32_t *col,
                         int64_t width, int64_t *num_blocks, int64_t *total_rows) {
-  if (width < 1) return 1;
+  if (width < 1 || ro[n] != m) return 1;
   int64_t B = (n + width - 1) / width, L = 0;
   for (int64_t v = 0; v < n; ++v) {
     int64_t prev = -1;
@@ -192,6 +192,7 @@ int orc_partition_fill(int64_t n, int64_t m, const int64_t *ro, const uint32_t *
                        const double *w, int64_t width, int64_t B,
                        int64_t *row_starts, int64_t *lro_arena, uint32_t *id_map,
                        int64_t *edge_starts, uint32_t *col_arena, double *w_arena) {
+  if (ro[n] != m) return 1;
   int64_t *epos = (int64_t *)calloc((size_t)(B + 1), sizeof(int64_t));
   int64_t *rpos = (int64_t *)calloc((size_t)(B + 1), sizeof(int64_t));
   if (!epos || !rpos) { free(epos); free(rpos); return 2; }
