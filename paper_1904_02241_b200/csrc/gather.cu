@@ -337,15 +337,9 @@ static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double 
   const int64_t lo = b * bg->width, hi = (lo + bg->width < bg->n) ? lo + bg->width : bg->n;
   const int hot = HOTBIT ? (int)bg->hot_k : (int)(bg->hot_k < hi - lo ? bg->hot_k : hi - lo);
   const size_t smem = (size_t)hot * 8 + kGWarps * 32 * sizeof(uint32_t);
-  static size_t done = 0;
-  if (smem > done) {
-    auto kern = k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps>;
-    GCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int pct = (int)(100.0 * carveout_kb() / 228.0 + 0.99);
-    GCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  pct > 100 ? 100 : pct));
-    done = smem;
-  }
+  const int pct = (int)(100.0 * carveout_kb() / 228.0 + 0.99);
+  ensure_smem_attrs(ctx, (const void *)k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps>, smem,
+                    pct > 100 ? 100 : pct);
   int64_t grid = ceil_div(nt, kGWarps);
   if (grid > ctx->num_sms) grid = ctx->num_sms;
   const double *hot_src = HOTBIT ? bg->hotval.p + b * bg->hot_k : vals + lo;

@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 #include <stdexcept>
 
@@ -217,6 +220,24 @@ struct DeviceGuard {
     if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
 };
+
+// Dynamic shared memory / carve-out attributes are per function and per
+// device: set them when a launch needs more than was set for this device, or
+// a different carve-out (carve_pct < 0 leaves the carve-out alone).
+inline void ensure_smem_attrs(gcb_ctx *ctx, const void *kern, size_t smem, int carve_pct = -1) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, std::pair<size_t, int>> set;
+  std::lock_guard<std::mutex> lock(mu);
+  auto &cur = set[{kern, ctx->device}];
+  if (smem > cur.first) {
+    GCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur.first = smem;
+  }
+  if (carve_pct >= 0 && carve_pct != cur.second) {
+    GCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve_pct));
+    cur.second = carve_pct;
+  }
+}
 
 inline void after_launch(gcb_ctx *ctx, const char *name) {
   ctx->launches++;

@@ -817,13 +817,9 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
     if (bg->hot_k > 0) {
       const int hot = (int)bg->hot_k;
       const size_t smem = (size_t)hot * sizeof(double);
-      static size_t done = 0;
-      if (smem > done) {
-        GCB_CUDA(cudaFuncSetAttribute(k_push_hot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        GCB_CUDA(cudaFuncSetAttribute(k_push_hot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        GCB_CUDA(cudaFuncSetAttribute(k_push_hot<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        done = smem;
-      }
+      ensure_smem_attrs(ctx, (const void *)k_push_hot<true>, smem);
+      ensure_smem_attrs(ctx, (const void *)k_push_hot<false>, smem);
+      ensure_smem_attrs(ctx, (const void *)k_push_hot<false, true>, smem);
       const unsigned gh = grid_for(nt * 32, 1024, (int64_t)ctx->num_sms);
       if (nonneg && !wgt && !getenv("GCB_NO_FIX"))
         k_push_hot<false, true><<<gh, 1024, smem, ctx->stream>>>(
