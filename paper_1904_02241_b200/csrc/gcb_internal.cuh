@@ -198,6 +198,9 @@ struct gcb_blocked {
   gcb::DArray<uint32_t> rl_perm;     // [n] original id -> renumbered id
   gcb_blocked *pending_hybrid = nullptr;  // build scratch of ensure_relabeled (owned)
 
+  // ---- tol > 0 PageRank: the convergence loop as one CUDA graph (pr.cu) ----
+  struct PrGraph *pr_graph = nullptr;  // owned
+
   gcb_blocked() = default;
   gcb_blocked(const gcb_blocked &) = delete;
   gcb_blocked &operator=(const gcb_blocked &) = delete;
@@ -323,6 +326,7 @@ void permute_in(gcb_ctx *ctx, const gcb_blocked *bg, const double *x, double *x_
 void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, double *y);
 int64_t hot_capacity(gcb_ctx *ctx);    // gather.cu: pull hot-table slots
 int64_t push_hot_slots(gcb_ctx *ctx);  // pr.cu: push hub-accumulator slots
+void destroy_pr_graph(struct ::PrGraph *g);  // pr.cu
 // partition.cu: conventional-blocking layout (the CB ablation)
 void to_cb_layout(gcb_ctx *ctx, gcb_blocked *bg);
 void cb_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights, bool exact,

@@ -309,6 +309,7 @@ gcb_blocked::~gcb_blocked() {
   delete rl;
   delete hybrid;
   delete pending_hybrid;
+  gcb::destroy_pr_graph(pr_graph);
 }
 
 namespace gcb {

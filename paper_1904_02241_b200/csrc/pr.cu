@@ -849,6 +849,126 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
   }
 }
 
+}  // namespace gcb
+
+// The tol > 0 convergence loop (kernels.py:257-266 / 397-404) as one CUDA graph:
+// a WHILE conditional node whose body is one iteration's launches plus
+// k_pr_check, which tests delta < tol on the device and sets the loop
+// condition, so iterations 2.. run with no host round trip (the host loop
+// read delta back after every iteration: +24 us per iteration at rmat:24).
+// The body is captured once per blocking and reused while the buffers it
+// was captured with stay the same.
+struct PrGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  gcb::DArray<int> state;  // [iterations run, converged, iteration budget]
+  const void *key[8] = {};
+  double kd[2] = {0, 0};
+  uint32_t kflags = 0;
+};
+
+namespace gcb {
+
+void destroy_pr_graph(PrGraph *g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+}
+
+__global__ void k_pr_check(cudaGraphConditionalHandle h, const double *__restrict__ delta,
+                           double tol, int *__restrict__ state) {
+  const int k = ++state[0];
+  const bool done = *delta < tol;
+  if (done) state[1] = 1;
+  cudaGraphSetConditional(h, (!done && k < state[2]) ? 1u : 0u);
+}
+
+static bool graph_loops_enabled(gcb_ctx *ctx) {
+  const char *env = getenv("GCB_NO_GRAPH");
+  return !ctx->profiling && !(env && env[0] && env[0] != '0');
+}
+
+// Runs up to `budget` more iterations of `iterate` inside one graph launch;
+// returns false (nothing run) when the graph cannot be built, and the caller
+// keeps the host loop.
+template <class F>
+static bool pr_graph_loop(gcb_ctx *ctx, gcb_blocked *bg, F &&iterate, const void *const key[8],
+                          double damping, double tol, uint32_t flags, const double *delta_dev,
+                          int budget, int *ran, int *conv) {
+  PrGraph *g = bg->pr_graph;
+  bool same = g && g->kd[0] == damping && g->kd[1] == tol && g->kflags == flags;
+  for (int i = 0; same && i < 8; ++i) same = g->key[i] == key[i];
+  if (!same) {
+    destroy_pr_graph(g);
+    bg->pr_graph = g = nullptr;
+    PrGraph *ng = new PrGraph();
+    cudaStream_t cs = nullptr, saved = ctx->stream;
+    bool ok = false, capturing = false;
+    try {
+      ng->state.alloc(3);
+      if (cudaGraphCreate(&ng->graph, 0) != cudaSuccess) throw 0;
+      cudaGraphConditionalHandle h;
+      if (cudaGraphConditionalHandleCreate(&h, ng->graph, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+        throw 0;
+      cudaGraphNodeParams p = {};
+      p.type = cudaGraphNodeTypeConditional;
+      p.conditional.handle = h;
+      p.conditional.type = cudaGraphCondTypeWhile;
+      p.conditional.size = 1;
+      cudaGraphNode_t node;
+      if (cudaGraphAddNode(&node, ng->graph, nullptr, 0, &p) != cudaSuccess) throw 0;
+      cudaGraph_t body = p.conditional.phGraph_out[0];
+      if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) throw 0;
+      if (cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeRelaxed) != cudaSuccess)
+        throw 0;
+      capturing = true;
+      ctx->stream = cs;
+      iterate();
+      k_pr_check<<<1, 1, 0, cs>>>(h, delta_dev, tol, ng->state.p);
+      after_launch(ctx, "k_pr_check");
+      ctx->stream = saved;
+      capturing = false;
+      if (cudaStreamEndCapture(cs, &body) != cudaSuccess) throw 0;
+      if (cudaGraphInstantiate(&ng->exec, ng->graph, 0) != cudaSuccess) throw 0;
+      ok = true;
+    } catch (...) {
+      // any failure (no conditional-node support, an operation the capture
+      // rejects): the caller keeps the host loop
+      ok = false;
+    }
+    ctx->stream = saved;
+    if (capturing) {
+      cudaGraph_t dropped = nullptr;
+      cudaStreamEndCapture(cs, &dropped);
+    }
+    if (cs) cudaStreamDestroy(cs);
+    if (!ok) {
+      destroy_pr_graph(ng);
+      cudaGetLastError();  // clear the (non-sticky) error of the failed build
+      return false;
+    }
+    for (int i = 0; i < 8; ++i) ng->key[i] = key[i];
+    ng->kd[0] = damping;
+    ng->kd[1] = tol;
+    ng->kflags = flags;
+    bg->pr_graph = g = ng;
+  }
+  int *hs = (int *)ctx->pinned;
+  hs[0] = 0;
+  hs[1] = 0;
+  hs[2] = budget;
+  GCB_CUDA(cudaMemcpyAsync(g->state.p, hs, 3 * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  GCB_CUDA(cudaGraphLaunch(g->exec, ctx->stream));
+  ctx->launches++;
+  GCB_CUDA(cudaMemcpyAsync(hs, g->state.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  *ran = hs[0];
+  *conv = hs[1];
+  return true;
+}
+
 // PageRank driver shared by pr_blocked / pr_baseline (kernels.py:207-268, 367-405)
 static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, int max_iters,
                    uint32_t flags, const uint32_t *deg_override, double *ranks_dev, int *iters,
@@ -891,9 +1011,8 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
                                                  bg->sums.p);
     after_launch(ctx, "k_pr_init");
   }
-  double *hdelta = (double *)ctx->pinned;
-  int it = 0, cv = 0;
-  for (int k = 0; k < max_iters; ++k) {
+  // one iteration's launches (no host synchronisation: also the graph body)
+  auto iterate = [&]() {
     if (!push) {
       pull_sums(ctx, bg, contrib, contrib32, false, flags, -1, bg->sums.p, true);
       if (bg->hybrid) {  // relabel.cu: cold-source -> hot-destination edges
@@ -912,15 +1031,35 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
       launch_update(ctx, exact, n, base, damping, bg->sums.p, ranks_dev, deg,
                     contrib ? contrib : (push ? bg->contrib.p : nullptr), contrib32, bg->deltas.p);
     }
-    ++it;
     if (tol > 0.0) {
       k_reduce_sum<<<1, 1024, 0, ctx->stream>>>(bg->deltas.p, update_grid(ctx, n), delta_dev);
       after_launch(ctx, "k_reduce_sum");
+    }
+  };
+  double *hdelta = (double *)ctx->pinned;
+  int it = 0, cv = 0;
+  for (int k = 0; k < max_iters; ++k) {
+    iterate();
+    ++it;
+    if (tol > 0.0) {
       d2h(ctx, hdelta, delta_dev, 1);
       sync(ctx);
       if (*hdelta < tol) {
         cv = 1;
         break;
+      }
+      // the first iteration built every lazy structure: the rest can loop on
+      // the device
+      if (k == 0 && max_iters > 1 && graph_loops_enabled(ctx)) {
+        const void *key[8] = {bg, ranks_dev, deg, contrib, contrib32, bg->sums.p, bg->deltas.p,
+                              bg->hybrid};
+        int ran = 0, c2 = 0;
+        if (pr_graph_loop(ctx, bg, iterate, key, damping, tol, flags, delta_dev, max_iters - 1,
+                          &ran, &c2)) {
+          it += ran;
+          cv = c2;
+          break;
+        }
       }
     }
   }
