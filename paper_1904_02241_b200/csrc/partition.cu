@@ -270,6 +270,13 @@ __global__ void k_compact_rows(int64_t Lb, const uint32_t *__restrict__ flag,
     if (flag[r]) out[pos[r]] = (uint32_t)r;
 }
 
+__global__ void k_row_lengths(int64_t c, const uint32_t *__restrict__ rows,
+                              const uint32_t *__restrict__ lro_b, uint32_t *__restrict__ len) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c;
+       i += (int64_t)gridDim.x * blockDim.x)
+    len[i] = lro_b[rows[i] + 1] - lro_b[rows[i]];
+}
+
 // bounds[b][j] = row_starts[b] + lower_bound(id_map_b, j*k), j in [0, R]
 __global__ void k_range_bounds(int64_t B, int64_t R, int64_t k, const int64_t *__restrict__ row_starts,
                                const uint32_t *__restrict__ id_map, int64_t *__restrict__ bounds) {
@@ -418,6 +425,18 @@ void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
       if (c) {
         k_compact_rows<<<grid_for(Lb, 256, 65536), 256, 0, ctx->stream>>>(Lb, lflag.p, lpos.p, part.p);
         after_launch(ctx, "k_compact_rows");
+        // longest first: the hub rows' add chains are the kernel's critical
+        // path, so their warps must start at once (rows are independent)
+        DArray<uint32_t> k1(c), k2(c), v2(c);
+        k_row_lengths<<<grid_for(c, 256, 65536), 256, 0, ctx->stream>>>(c, part.p, bg->lro.p + rs + b,
+                                                                       k1.p);
+        after_launch(ctx, "k_row_lengths");
+        uint32_t *rk = nullptr, *rv = nullptr;
+        cub_sort_pairs_desc_u32_u32(ctx, k1.p, k2.p, part.p, v2.p, c, &rk, &rv);
+        if (rv != part.p)
+          GCB_CUDA(cudaMemcpyAsync(part.p, rv, c * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+        sync(ctx);  // k1/k2/v2 are released at scope end
       }
       parts.push_back(std::move(part));
       total += c;

@@ -243,37 +243,66 @@ __global__ void k_pull_exact_long(const uint32_t *__restrict__ col_b, const doub
                                   const uint32_t *__restrict__ id_map_b,
                                   const uint32_t *__restrict__ long_rows, int64_t nlong,
                                   const double *__restrict__ vals, double *__restrict__ out) {
-  const unsigned FULL = 0xffffffffu;
+  __shared__ double s_buf[8][256];  // one 256-value slot per warp (256-thread CTAs)
+  double *buf = s_buf[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nlong; j += nw) {
     const uint32_t i = long_rows[j];
     const uint32_t b0 = lro_b[i], b1 = lro_b[i + 1];
     double acc = 0.0;
-    // 8 chunks of 32 edges per step: the 8 gathers of a lane are in flight
-    // together, then the 256 values are added in edge order
-    for (uint32_t base = b0; base < b1; base += 256) {
-      double x[8];
+    // Steps of 256 edges (8 per lane).  Software pipeline over steps: the
+    // column ids of step s+2 and the gathered values of step s+1 are in
+    // flight while step s's 256 values are added in edge order, so neither
+    // the col load nor the value gather sits in front of the add chain -- the
+    // chain (8.7 cycles per f64 add, scripts/mb_dadd.cu) is the hub rows'
+    // critical path.  The step's values go through the warp's shared-memory
+    // slot, read back with independent LDS (a SHFL per add sat on the chain).
+    constexpr uint32_t kNone = 0xffffffffu;
+    auto load_cols = [&](uint32_t base, uint32_t (&c)[8], double (&w)[8]) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint32_t e = base + q * 32 + lane;
-        x[q] = 0.0;
-        if (e < b1) {
-          x[q] = vals[col_b[e]];
-          if (WGT) x[q] = __dmul_rn(w_b[e], x[q]);
-        }
+        c[q] = e < b1 ? col_b[e] : kNone;
+        if (WGT) w[q] = e < b1 ? w_b[e] : 0.0;
       }
+    };
+    auto load_vals = [&](const uint32_t (&c)[8], const double (&w)[8], double (&x)[8]) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const uint32_t cb = base + q * 32;
-        if (cb >= b1) break;
-        const int cnt = (int)(b1 - cb < 32u ? b1 - cb : 32u);
-        if (cnt == 32) {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) acc = __dadd_rn(acc, __shfl_sync(FULL, x[q], k));
-        } else {
-          for (int k = 0; k < cnt; ++k) acc = __dadd_rn(acc, __shfl_sync(FULL, x[q], k));
+        x[q] = 0.0;
+        if (c[q] != kNone) {
+          x[q] = vals[c[q]];
+          if (WGT) x[q] = __dmul_rn(w[q], x[q]);
         }
+      }
+    };
+    uint32_t c1[8], c2[8];
+    double w1[8], w2[8], x[8], nx[8];
+    load_cols(b0, c1, w1);
+    load_vals(c1, w1, x);                 // step 0
+    load_cols(b0 + 256, c1, w1);          // step 1's columns
+    for (uint32_t base = b0; base < b1; base += 256) {
+      if (base + 256 < b1) {
+        load_vals(c1, w1, nx);            // step s+1 (columns arrived a step ago)
+        load_cols(base + 512, c2, w2);    // step s+2
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) buf[q * 32 + lane] = x[q];
+      __syncwarp();
+      const int cnt = (int)(b1 - base < 256u ? b1 - base : 256u);
+      if (cnt == 256) {
+#pragma unroll 64
+        for (int k = 0; k < 256; ++k) acc = __dadd_rn(acc, buf[k]);
+      } else {
+        for (int k = 0; k < cnt; ++k) acc = __dadd_rn(acc, buf[k]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        x[q] = nx[q];
+        c1[q] = c2[q];
+        if (WGT) w1[q] = w2[q];
       }
     }
     if (lane == 0) exact_store<WGT, ACCUM>(out, id_map_b, i, acc);
