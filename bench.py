@@ -196,8 +196,8 @@ def workload_config(args, n, m):
         "iterations_per_step": args.iters, "damping": 0.85, "tol": 0.0,
         "direction": args.direction, "value_dtype": "f32" if args.f32_values else "f64",
         "l2": "inputs larger than L2 (col arena 4|E| bytes >> 126 MB)",
-        "parallelism": (f"destination shards x{args.gpus} (cuts balance in-edges + 4 x vertices), NCCL all_to_all of "
-                        "the contributions each shard reads" if args.gpus > 1 else "single GPU"),
+        "parallelism": (f"destination shards x{args.gpus} (cuts balance in-edges + 4 x vertices), "
+                        "contribution exchange per config.exchange" if args.gpus > 1 else "single GPU"),
     }
 
 
@@ -253,7 +253,17 @@ def run_ours(args):
         plan = parallel.ShardPlan(parallel.shard_ranges(src.row_offsets, world))
         # width 0: size each shard's blocks from the sources its slab reads
         engine = parallel.DeviceShard(src, *plan.owned(rank), 0, flags)
-        exchange = parallel.SparseExchange(plan, rank, engine.source_mask())
+        # default: the exchange fused into the rank update over peer memory
+        # (csrc/exchange.cu); GCB_EXCHANGE=nccl selects the sparse NCCL
+        # all_to_all, which is also the fallback when peer mapping fails
+        exchange = None
+        if os.environ.get("GCB_EXCHANGE", "p2p") == "p2p":
+            try:
+                exchange = parallel.PeerExchange(engine, plan, rank)
+            except RuntimeError as e:
+                print(f"peer exchange unavailable ({e}); using NCCL all_to_all", file=sys.stderr)
+        if exchange is None:
+            exchange = parallel.SparseExchange(plan, rank, engine.source_mask())
         runner = parallel.ShardedPageRank(engine, plan, rank, exchange)
         n, m = src.num_vertices, src.num_edges
         bg = engine.bg
@@ -383,7 +393,12 @@ def run_ours(args):
     cfg = workload_config(args, n, m)
     if world > 1:
         cfg["width"] = int(bg.width)  # rank 0's shard width (auto: DeviceShard._auto_width)
-        cfg["exchange_bytes_received_rank0"] = int(exchange.bytes_received)
+        if getattr(exchange, "fused", False):
+            cfg["exchange"] = "peer-memory stores fused into the rank update (CUDA IPC / NVLink)"
+            cfg["exchange_bytes_stored_rank0"] = int(exchange.bytes_per_step)
+        else:
+            cfg["exchange"] = "NCCL all_to_all_single of the contributions each shard reads"
+            cfg["exchange_bytes_received_rank0"] = int(exchange.bytes_received)
     if rank == 0:
         line = {
             "metric": "PageRank GTEPS per iteration", "value": round(value, 3), "unit": "GTEPS",

@@ -183,6 +183,33 @@ int gcb_pr_shard_init(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1,
 int gcb_pr_shard_step(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, double damping,
                       uint32_t flags, const uint32_t *deg_dev, double *contrib_dev,
                       double *ranks_dev, double *delta_dev);
+/* The same step with the contribution exchange fused into the update over
+ * peer memory (csrc/exchange.cu), replacing the NCCL exchange between
+ * gcb_pr_shard_step calls.  Buffers come from gcb_ipc_alloc and are mapped in
+ * every rank with gcb_ipc_open (CUDA IPC; NVLink P2P across GPUs).
+ *   out_dev[p]   device array of num_ranks pointers: rank p's contribution
+ *                buffer of this epoch's parity (the caller alternates two)
+ *   need_dev     uint8[v1 - v0]: bit p = rank p's slab reads that source
+ *   flags_dev[p] device array of num_ranks pointers to each rank's uint32[P]
+ *                epoch flags; my_flags_dev is this rank's own
+ * init publishes epoch `epoch`; step waits for every peer's epoch - 1,
+ * gathers contrib_in (the other buffer), updates the owned slice, stores each
+ * contribution into the peers that read it and publishes `epoch`.  Stream-
+ * ordered, no host synchronisation; a peer that never publishes makes the
+ * wait kernel trap after ~20 s instead of hanging the device. */
+int gcb_ipc_alloc(gcb_ctx *ctx, int64_t bytes, void **ptr, unsigned char *handle64);
+int gcb_ipc_free(gcb_ctx *ctx, void *ptr);
+int gcb_ipc_open(gcb_ctx *ctx, const unsigned char *handle64, void **ptr);
+int gcb_ipc_close(gcb_ctx *ctx, void *ptr);
+int gcb_pr_shard_init_p2p(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1,
+                          const uint32_t *deg_dev, double *ranks_dev, double *const *out_dev,
+                          const uint8_t *need_dev, int num_ranks, int rank,
+                          uint32_t *const *flags_dev, uint32_t epoch);
+int gcb_pr_shard_step_p2p(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, double damping,
+                          uint32_t flags, const uint32_t *deg_dev, const double *contrib_in,
+                          double *ranks_dev, double *delta_dev, double *const *out_dev,
+                          const uint8_t *need_dev, int num_ranks, int rank,
+                          uint32_t *const *flags_dev, uint32_t *my_flags_dev, uint32_t epoch);
 /* process_block_pull kernels.py:275-282: partials of block b (n_local f64) */
 int gcb_process_block_pull(gcb_ctx *ctx, gcb_blocked *bg, int64_t block,
                            const double *contrib_host, uint32_t flags,

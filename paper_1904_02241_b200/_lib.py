@@ -64,6 +64,14 @@ SIGNATURES = {
     "gcb_csr_col_counts": ([c_vp, c_vp, c_vp], c_int),
     "gcb_pr_shard_init": ([c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp], c_int),
     "gcb_pr_shard_step": ([c_vp, c_vp, c_i64, c_i64, c_dbl, c_u32, c_vp, c_vp, c_vp, c_vp], c_int),
+    "gcb_ipc_alloc": ([c_vp, c_i64, PP, c_vp], c_int),
+    "gcb_ipc_free": ([c_vp, c_vp], c_int),
+    "gcb_ipc_open": ([c_vp, c_vp, PP], c_int),
+    "gcb_ipc_close": ([c_vp, c_vp], c_int),
+    "gcb_pr_shard_init_p2p": ([c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_int, c_int,
+                               c_vp, c_u32], c_int),
+    "gcb_pr_shard_step_p2p": ([c_vp, c_vp, c_i64, c_i64, c_dbl, c_u32, c_vp, c_vp, c_vp, c_vp,
+                               c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_u32], c_int),
     "gcb_csr_destroy": ([c_vp], c_int),
     "gcb_partition_tocab": ([c_vp, c_vp, c_int, c_i64, PP], c_int),
     "gcb_partition_cb": ([c_vp, c_vp, c_i64, PP], c_int),

@@ -34,6 +34,7 @@ namespace gcb {
 }  // namespace gcb
 
 #include "ldst.cuh"
+#include "pr_math.cuh"
 #include "tiles.cuh"
 
 namespace gcb {
@@ -378,34 +379,8 @@ __global__ void k_pr_init(int64_t n, double r0, const uint32_t *__restrict__ deg
 
 // rank update (kernels.py:398-399) fused with the L1 delta (399), the next
 // iteration's contributions (185-191) and clearing sums for the next pass.
-// Rank update, persistent form: 2 CTAs x 512 threads per SM, each thread
-// streams two 4-vertex quads per step (10 x 16-byte loads in flight) and the
-// CTA reduces its delta once at the end.  (ncu on the one-quad-per-thread
-// form: 80 registers, 36% occupancy, 47% of stalls on the per-CTA barrier,
-// 34% of DRAM peak.)  Fast mode replaces the IEEE divide by deg with a
-// Newton-refined reciprocal (<= 2 ulp; the exact mode keeps __ddiv_rn).
-template <bool EXACT>
-__device__ __forceinline__ double div_deg(double r, uint32_t dg) {
-  if (EXACT) return __ddiv_rn(r, (double)dg);
-  const double d = (double)dg;
-  double q = (double)__frcp_rn((float)dg);
-  q = fma(fma(-d, q, 1.0), q, q);
-  q = fma(fma(-d, q, 1.0), q, q);
-  return r * q;
-}
-
-template <bool EXACT>
-__device__ __forceinline__ void pr_quad(const double *s, const double *o, const uint4 d, double base,
-                                        double damping, double *nr, double *c, double &dsum) {
-  const uint32_t dg[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    nr[k] = __dadd_rn(base, __dmul_rn(damping, s[k]));
-    dsum += fabs(nr[k] - o[k]);
-    c[k] = dg[k] ? div_deg<EXACT>(nr[k], dg[k]) : 0.0;
-  }
-}
-
+// One 4-vertex quad per thread (update_grid): 256-bit loads and stores, the
+// CTA reduces its delta once at the end.  The arithmetic is pr_math.cuh's.
 template <bool EXACT>
 __global__ void __launch_bounds__(512, 2)
     k_pr_update2(int64_t n, double base, double damping, double *__restrict__ sums,

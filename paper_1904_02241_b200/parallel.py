@@ -31,8 +31,8 @@ from .blocking import BlockedGraph, partition_tocab
 from .graph import CsrGraph
 from .kernels import PrParams, PrResult
 
-__all__ = ["shard_ranges", "DeviceShard", "TorchExchange", "SparseExchange", "LoopbackExchange",
-           "ShardedPageRank", "sharded_pagerank_virtual"]
+__all__ = ["shard_ranges", "DeviceShard", "TorchExchange", "SparseExchange", "PeerExchange",
+           "LoopbackExchange", "ShardedPageRank", "sharded_pagerank_virtual"]
 
 
 # Cost of one owned vertex relative to one in-edge in a shard's step: the
@@ -98,11 +98,14 @@ class TorchExchange:
     def _buffers(self, full):
         import torch
 
-        key = (full.device, full.dtype)
+        # the collective runs where the backend wants its tensors (CPU for
+        # gloo, which cannot all-gather CUDA tensors); copies stage through
+        dev = _coll_device(self.group) if full.is_cuda else full.device
+        key = (dev, full.dtype)
         if key not in self._buf:
             P, L = self.plan.parts, self.plan.max_len
-            self._buf[key] = (torch.zeros(L, dtype=full.dtype, device=full.device),
-                              torch.zeros(P * L, dtype=full.dtype, device=full.device))
+            self._buf[key] = (torch.zeros(L, dtype=full.dtype, device=dev),
+                              torch.zeros(P * L, dtype=full.dtype, device=dev))
         return self._buf[key]
 
     def sync(self, full):
@@ -122,7 +125,8 @@ class TorchExchange:
         import torch
         import torch.distributed as dist
 
-        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dev = _coll_device(self.group) if torch.device(device).type == "cuda" else device
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, group=self.group)
         return float(t.item())
 
@@ -190,6 +194,134 @@ class SparseExchange:
 
     def allreduce_sum(self, x: float, device) -> float:
         return self.full.allreduce_sum(x, device)
+
+
+def _coll_device(group=None):
+    """Where torch.distributed wants collective tensors: CUDA for NCCL, else CPU."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+class PeerExchange:
+    """The contribution exchange fused into the rank update over peer memory
+    (csrc/exchange.cu): every rank exports two contribution buffers and a
+    row of epoch flags by CUDA IPC and maps everyone else's; the update kernel
+    stores each owned contribution straight into the buffers of the ranks
+    whose slabs read it (NVLink P2P stores) and publishes its epoch, and the
+    next step waits on the peers' epochs on the device.  No NCCL call and no
+    host synchronisation inside the iteration loop.
+
+    Setup (once): IPC handles are swapped with all_gather_object, and the
+    per-owned-vertex need masks (bit p = rank p's slab reads v) come from one
+    all-gather of the ranks' source masks.  Up to 8 ranks (one node)."""
+
+    fused = True
+
+    def __init__(self, engine: "DeviceShard", plan: ShardPlan, rank: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        P = plan.parts
+        if P > 8:
+            raise ValueError("the peer exchange supports up to 8 ranks (one node)")
+        self.plan, self.rank, self.group = plan, rank, group
+        self.full = TorchExchange(plan, rank, group)  # final ranks gather, scalar reductions
+        ctx = engine.ctx
+        self.ctx = ctx
+        n, dev = engine.n, engine.device
+        self._own, self._opened, self._closed = [], [], False
+        handles = []
+        for nbytes in (8 * n, 8 * n, 4 * P):  # contribution buffers 0/1, epoch flags
+            ptr = ctypes.c_void_p()
+            h = (ctypes.c_ubyte * 64)()
+            _lib.check(ctx._lib.gcb_ipc_alloc(ctx.handle, nbytes, ctypes.byref(ptr), h), "ipc alloc")
+            self._own.append(int(ptr.value))
+            handles.append(bytes(h))
+        everyone = [None] * P
+        dist.all_gather_object(everyone, handles, group=group)
+        ptrs = [[0, 0, 0] for _ in range(P)]
+        ok = 1
+        try:
+            for q in range(P):
+                for k in range(3):
+                    if q == rank:
+                        ptrs[q][k] = self._own[k]
+                        continue
+                    p = ctypes.c_void_p()
+                    hb = (ctypes.c_ubyte * 64).from_buffer_copy(everyone[q][k])
+                    _lib.check(ctx._lib.gcb_ipc_open(ctx.handle, hb, ctypes.byref(p)), "ipc open")
+                    self._opened.append(int(p.value))
+                    ptrs[q][k] = int(p.value)
+        except (RuntimeError, ValueError, MemoryError):  # _lib.GcbError is a RuntimeError
+            ok = 0
+        # every rank learns whether every rank mapped every peer, so all take
+        # the same exchange
+        flag = torch.tensor([ok], dtype=torch.int32, device=_coll_device(group))
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if not int(flag.item()):
+            self.close()
+            raise RuntimeError("CUDA IPC mapping of a peer's buffers failed on some rank")
+        self.out_tab = [torch.tensor([ptrs[q][k] for q in range(P)], dtype=torch.int64, device=dev)
+                        for k in (0, 1)]
+        self.flag_tab = torch.tensor([ptrs[q][2] for q in range(P)], dtype=torch.int64, device=dev)
+        # need[v - v0] bit p: rank p (p != self) reads owned vertex v
+        cd = _coll_device(group)
+        mine = engine.source_mask().to(torch.uint8).to(cd)
+        masks = [torch.empty_like(mine) for _ in range(P)]
+        dist.all_gather(masks, mine, group=group)
+        v0, v1 = plan.owned(rank)
+        cnt = v1 - v0
+        need = torch.zeros(((cnt + 3) // 4) * 4 or 4, dtype=torch.uint8, device=dev)
+        for p in range(P):
+            if p != rank and cnt:
+                need[:cnt] |= (masks[p][v0:v1].to(dev) << p).to(torch.uint8)
+        self.need = need
+        self.epoch = 0
+        popc = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int64, device=dev)
+        self.bytes_per_step = 8 * int(popc[need[:cnt].long()].sum()) if cnt else 0  # P2P stores
+
+    def buffer(self, epoch: int) -> int:
+        return self._own[epoch % 2]
+
+    def begin(self) -> int:
+        """Quiesce every rank's previous work (peers write into our buffers),
+        then hand out the next epoch for init."""
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        self.epoch += 1
+        return self.epoch
+
+    def end(self, epoch: int):
+        self.epoch = epoch
+
+    def sync_full(self, full):
+        self.full.sync(full)
+
+    def allreduce_sum(self, x: float, device) -> float:
+        return self.full.allreduce_sum(x, device)
+
+    def close(self):
+        """Unmap the peers' buffers, then free ours once every rank has unmapped."""
+        import torch
+        import torch.distributed as dist
+
+        if self._closed:
+            return
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        for p in self._opened:
+            _lib.check(self.ctx._lib.gcb_ipc_close(self.ctx.handle, ctypes.c_void_p(p)), "ipc close")
+        dist.barrier(group=self.group)
+        for p in self._own:
+            _lib.check(self.ctx._lib.gcb_ipc_free(self.ctx.handle, ctypes.c_void_p(p)), "ipc free")
+        self._opened, self._own, self._closed = [], [], True
 
 
 class LoopbackExchange:
@@ -276,6 +408,26 @@ class DeviceShard:
             ctypes.c_void_p(self.deg.data_ptr()), ctypes.c_void_p(contrib.data_ptr()),
             ctypes.c_void_p(ranks.data_ptr())), "shard init")
 
+    def init_p2p(self, ranks, ex: PeerExchange, epoch: int):
+        P = ex.plan.parts
+        _lib.check(self.ctx._lib.gcb_pr_shard_init_p2p(
+            self.ctx.handle, self.bg.device().raw, self.v0, self.v1,
+            ctypes.c_void_p(self.deg.data_ptr()), ctypes.c_void_p(ranks.data_ptr()),
+            ctypes.c_void_p(ex.out_tab[epoch % 2].data_ptr()), ctypes.c_void_p(ex.need.data_ptr()),
+            P, ex.rank, ctypes.c_void_p(ex.flag_tab.data_ptr()), epoch & 0xFFFFFFFF), "shard init p2p")
+
+    def step_p2p(self, ranks, ex: PeerExchange, epoch: int, damping: float, want_delta: bool):
+        P = ex.plan.parts
+        _lib.check(self.ctx._lib.gcb_pr_shard_step_p2p(
+            self.ctx.handle, self.bg.device().raw, self.v0, self.v1, float(damping), self.flags,
+            ctypes.c_void_p(self.deg.data_ptr()), ctypes.c_void_p(ex.buffer(epoch - 1)),
+            ctypes.c_void_p(ranks.data_ptr()),
+            ctypes.c_void_p(self.delta.data_ptr()) if want_delta else None,
+            ctypes.c_void_p(ex.out_tab[epoch % 2].data_ptr()), ctypes.c_void_p(ex.need.data_ptr()),
+            P, ex.rank, ctypes.c_void_p(ex.flag_tab.data_ptr()), ctypes.c_void_p(ex._own[2]),
+            epoch & 0xFFFFFFFF), "shard step p2p")
+        return self.delta if want_delta else None
+
     def step(self, contrib, ranks, damping: float, want_delta: bool):
         _lib.check(self.ctx._lib.gcb_pr_shard_step(
             self.ctx.handle, self.bg.device().raw, self.v0, self.v1, float(damping), self.flags,
@@ -295,6 +447,8 @@ class ShardedPageRank:
         self.exchange = exchange
 
     def run(self, params: PrParams = PrParams(), gather_ranks: bool = True) -> PrResult:
+        if getattr(self.exchange, "fused", False):
+            return self._run_fused(params, gather_ranks)
         import torch
 
         eng = self.engine
@@ -315,6 +469,30 @@ class ShardedPageRank:
                     break
         if gather_ranks:
             getattr(self.exchange, "sync_full", self.exchange.sync)(ranks)
+        return PrResult(ranks, it, conv)
+
+
+    def _run_fused(self, params: PrParams, gather_ranks: bool) -> PrResult:
+        """The loop over PeerExchange: init publishes epoch e0, step e waits
+        for e - 1, gathers buffer (e-1) % 2 and writes buffer e % 2."""
+        import torch
+
+        eng, ex = self.engine, self.exchange
+        ranks = torch.zeros(eng.n, dtype=torch.float64, device=eng.device)
+        e = ex.begin()
+        eng.init_p2p(ranks, ex, e)
+        it, conv = 0, False
+        for _ in range(params.max_iters):
+            e += 1
+            d = eng.step_p2p(ranks, ex, e, params.damping, params.tol > 0.0)
+            it += 1
+            if params.tol > 0.0:
+                if ex.allreduce_sum(float(d.item()), eng.device) < params.tol:
+                    conv = True
+                    break
+        ex.end(e)
+        if gather_ranks:
+            ex.sync_full(ranks)
         return PrResult(ranks, it, conv)
 
 
