@@ -866,7 +866,8 @@ struct PrGraph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   gcb::DArray<int> state;  // [iterations run, converged, iteration budget]
-  const void *key[8] = {};
+  static constexpr int kKey = 16;
+  const void *key[kKey] = {};
   double kd[2] = {0, 0};
   uint32_t kflags = 0;
 };
@@ -897,12 +898,12 @@ static bool graph_loops_enabled(gcb_ctx *ctx) {
 // returns false (nothing run) when the graph cannot be built, and the caller
 // keeps the host loop.
 template <class F>
-static bool pr_graph_loop(gcb_ctx *ctx, gcb_blocked *bg, F &&iterate, const void *const key[8],
+static bool pr_graph_loop(gcb_ctx *ctx, gcb_blocked *bg, F &&iterate, const void *const *key,
                           double damping, double tol, uint32_t flags, const double *delta_dev,
                           int budget, int *ran, int *conv) {
   PrGraph *g = bg->pr_graph;
   bool same = g && g->kd[0] == damping && g->kd[1] == tol && g->kflags == flags;
-  for (int i = 0; same && i < 8; ++i) same = g->key[i] == key[i];
+  for (int i = 0; same && i < PrGraph::kKey; ++i) same = g->key[i] == key[i];
   if (!same) {
     destroy_pr_graph(g);
     bg->pr_graph = g = nullptr;
@@ -953,7 +954,7 @@ static bool pr_graph_loop(gcb_ctx *ctx, gcb_blocked *bg, F &&iterate, const void
       cudaGetLastError();  // clear the (non-sticky) error of the failed build
       return false;
     }
-    for (int i = 0; i < 8; ++i) ng->key[i] = key[i];
+    for (int i = 0; i < PrGraph::kKey; ++i) ng->key[i] = key[i];
     ng->kd[0] = damping;
     ng->kd[1] = tol;
     ng->kflags = flags;
@@ -1055,8 +1056,15 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
       // the first iteration built every lazy structure: the rest can loop on
       // the device
       if (k == 0 && max_iters > 1 && graph_loops_enabled(ctx)) {
-        const void *key[8] = {bg, ranks_dev, deg, contrib, contrib32, bg->sums.p, bg->deltas.p,
-                              bg->hybrid};
+        // every buffer the captured launches read or write: a rebuilt layout
+        // (other table sizes, say) or another output vector means a new graph
+        const gcb_blocked *hy = bg->hybrid;
+        const void *key[PrGraph::kKey] = {bg, ranks_dev, deg, contrib, contrib32, bg->sums.p,
+                                          bg->deltas.p, hy, bg->xcol.p, bg->hotval.p,
+                                          bg->hot_ids.p, bg->rstart.p, bg->tile_row.p,
+                                          (const void *)(intptr_t)bg->hot_k,
+                                          hy ? hy->xcol.p : nullptr,
+                                          hy ? (const void *)(intptr_t)hy->hot_k : nullptr};
         int ran = 0, c2 = 0;
         if (pr_graph_loop(ctx, bg, iterate, key, damping, tol, flags, delta_dev, max_iters - 1,
                           &ran, &c2)) {
