@@ -107,6 +107,8 @@ struct gcb_ctx {
   int64_t launches = 0;
   void *pinned = nullptr;  // small pinned host staging (scalars)
   cudaStream_t copy_stream = nullptr;  // host->device copies overlapped with kernels
+  cudaStream_t aux_stream = nullptr;   // second compute stream (exact pull: blocks 1..B-1)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   gcb::DArray<uint8_t> cub_tmp;
   gcb::DArray<uint8_t> scratch;  // general scratch
   // optional per-category kernel timing (gcb_ctx_set_profiling)

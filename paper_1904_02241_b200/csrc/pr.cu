@@ -771,6 +771,53 @@ void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *v
   }
 }
 
+void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out);
+
+// Exact pull pass of a multi-block graph into zeroed sums.  Accumulating
+// block by block serialises the blocks' long-row kernels, and each is bound by
+// its hub row's dependent add chain (rmat:24: 2.26 + 0.73 ms).  Instead every
+// block writes its partials (the same per-row sums) to the partials arena --
+// block 0 on the main stream, the others on the auxiliary stream, so the
+// chains overlap -- and the block-ordered merge (k_merge, accumulate_ranges
+// kernels.py:300-321) forms ((0 + p_0) + p_1) + ..., the value accumulating
+// into zeroed sums gives, bit for bit.
+static void exact_pull_concurrent(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool wgt,
+                                  double *out) {
+  bg->partials.ensure(bg->L ? bg->L : 1);
+  if (!ctx->aux_stream) {
+    GCB_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+    GCB_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    GCB_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+  }
+  GCB_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+  GCB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->fork_ev, 0));
+  for (int64_t b = 0; b < bg->B; ++b) {
+    const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+    if (Lb == 0) continue;
+    cudaStream_t st = b == 0 ? ctx->stream : ctx->aux_stream;
+    const int64_t es = bg->h_edge_starts[b];
+    const uint32_t *lro_b = bg->lro.p + rs + b;
+    const uint32_t *idm_b = bg->id_map.p + rs;
+    const double *wb = wgt ? bg->w.p + es : nullptr;
+    double *o = bg->partials.p + rs;
+    const uint32_t *lr = bg->long_rows.p + bg->h_long_base[b];
+    const int64_t nl = bg->h_long_base[b + 1] - bg->h_long_base[b];
+    const unsigned g = grid_for(Lb, 256, (int64_t)ctx->num_sms * 16);
+    const unsigned gl = grid_for(nl * 32, 256, (int64_t)ctx->num_sms * 16);
+    if (wgt) {
+      k_pull_exact<true, false><<<g, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
+      if (nl) k_pull_exact_long<true, false><<<gl, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+    } else {
+      k_pull_exact<false, false><<<g, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
+      if (nl) k_pull_exact_long<false, false><<<gl, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+    }
+    after_launch(ctx, "k_pull_exact");
+  }
+  GCB_CUDA(cudaEventRecord(ctx->join_ev, ctx->aux_stream));
+  GCB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+  merge_to(ctx, bg, out);
+}
+
 void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out) {
   ensure_derived(ctx, bg);
   if (bg->R == 0) return;
@@ -1018,7 +1065,10 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   }
   // one iteration's launches (no host synchronisation: also the graph body)
   auto iterate = [&]() {
-    if (!push) {
+    if (!push && exact && !bg->cb && bg->B > 1 && contrib) {
+      ProfScope ps(ctx, 0);
+      exact_pull_concurrent(ctx, bg, contrib, false, bg->sums.p);
+    } else if (!push) {
       pull_sums(ctx, bg, contrib, contrib32, false, flags, -1, bg->sums.p, true);
       if (bg->hybrid) {  // relabel.cu: cold-source -> hot-destination edges
         ProfScope ps(ctx, 0);
