@@ -277,10 +277,16 @@ __global__ void k_seed(int64_t src, int32_t *depth, uint32_t *queue, uint32_t *b
   bits[src >> 5] = 1u << (src & 31);
 }
 
+// levels_host (optional, pinned): each committed level's queue slice is copied
+// back on the copy stream while the next level runs (the caller waits for the
+// copy stream)
 static void bfs_run(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int64_t source, int mode,
                     int64_t capacity, int64_t value_bytes, int32_t *depth_dev, uint32_t *levels_dev,
-                    std::vector<int64_t> &level_sizes, std::vector<uint8_t> &dirs) {
+                    std::vector<int64_t> &level_sizes, std::vector<uint8_t> &dirs,
+                    uint32_t *levels_host = nullptr) {
   const int64_t n = g->n;
+  if (levels_host && !ctx->copy_stream)
+    GCB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   Frontier F(n);
   k_fill_i32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, kInfDepth, depth_dev);
   after_launch(ctx, "k_fill_i32");
@@ -326,6 +332,15 @@ static void bfs_run(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int64_t sou
     int64_t cnt = 0;
     uint64_t ds = 0;
     commit_level(ctx, g, F, level + 1, levels_dev + qoff + qsize, depth_dev, &cnt, &ds);
+    if (levels_host) {
+      // commit_level synchronised the stream: the slice is final
+      if (qoff == 0)
+        GCB_CUDA(cudaMemcpyAsync(levels_host, levels_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                 ctx->copy_stream));
+      if (cnt)
+        GCB_CUDA(cudaMemcpyAsync(levels_host + qoff + qsize, levels_dev + qoff + qsize,
+                                 cnt * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->copy_stream));
+    }
     qoff += qsize;
     qsize = cnt;
     work = ds;
@@ -530,12 +545,11 @@ int gcb_bfs(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t source
     DArray<uint32_t> levels(g->n ? g->n : 1);
     std::vector<int64_t> sizes;
     std::vector<uint8_t> dirs;
-    bfs_run(ctx, g, bg, source, mode, capacity_bytes, value_bytes, depth.p, levels.p, sizes, dirs);
-    int64_t total = 0;
-    for (auto s : sizes) total += s;
+    bfs_run(ctx, g, bg, source, mode, capacity_bytes, value_bytes, depth.p, levels.p, sizes, dirs,
+            level_verts_host);
     d2h(ctx, depth_host, depth.p, g->n);
-    if (level_verts_host) d2h(ctx, level_verts_host, levels.p, total);
     sync(ctx);
+    if (level_verts_host) GCB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
     *num_levels = (int64_t)sizes.size();
     *num_expansions = (int64_t)dirs.size();
     for (int64_t i = 0; i < (int64_t)sizes.size() && i < max_levels; ++i) {
