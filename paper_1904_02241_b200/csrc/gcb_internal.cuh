@@ -324,7 +324,6 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
 // relabel.cu: degree-ordered execution copy of a pull graph
 bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters);
 gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg);
-void permute_in(gcb_ctx *ctx, const gcb_blocked *bg, const double *x, double *x_new);
 void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, double *y);
 int64_t hot_capacity(gcb_ctx *ctx);    // gather.cu: pull hot-table slots
 int64_t push_hot_slots(gcb_ctx *ctx);  // pr.cu: push hub-accumulator slots

@@ -294,12 +294,6 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
   return bg->rl;
 }
 
-void permute_in(gcb_ctx *ctx, const gcb_blocked *bg, const double *x, double *x_new) {
-  k_permute_in<double><<<grid_for(bg->n, 256, 65536), 256, 0, ctx->stream>>>(bg->n, bg->rl_perm.p,
-                                                                            x, x_new);
-  after_launch(ctx, "k_permute_in");
-}
-
 void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, double *y) {
   k_permute_out<double><<<grid_for(bg->n, 256, 65536), 256, 0, ctx->stream>>>(bg->n, bg->rl_perm.p,
                                                                              y_new, y);
