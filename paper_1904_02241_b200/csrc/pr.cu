@@ -1281,7 +1281,6 @@ static void pull_spmv(gcb_ctx *ctx, gcb_blocked *bg, const double *x, bool weigh
                       double *y) {
   GCB_CUDA(cudaMemsetAsync(y, 0, (bg->n ? bg->n : 1) * sizeof(double), ctx->stream));
   pull_sums(ctx, bg, x, nullptr, weights, flags, -1, y, true);
-  if (bg->hybrid) push_scatter(ctx, bg->hybrid, x, y, weights, flags, -1);
 }
 
 int gcb_segment_row_sums(gcb_ctx *ctx, const gcb_csr *g, const double *values_host, int use_weights,
