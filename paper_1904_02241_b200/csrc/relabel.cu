@@ -200,7 +200,7 @@ int64_t hybrid_split(gcb_ctx *ctx, gcb_blocked *bg, DArray<uint32_t> &rows, DArr
 
 bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters) {
   if (flags & (GCB_FLAG_EXACT | GCB_FLAG_NO_RELABEL)) return false;
-  if (bg->direction != 0 || bg->m == 0 || bg->n >= (int64_t(1) << 32)) return false;
+  if (bg->m == 0 || bg->n >= (int64_t(1) << 32)) return false;
   if (bg->is_relabeled || bg->cb) return false;
   const char *env = getenv("GCB_NO_RELABEL");
   if (env && env[0] && env[0] != '0') return false;
@@ -242,6 +242,9 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
           cols.p + es);
       after_launch(ctx, "k_relabel_block");
     }
+    // a push blocking's rows are sources: the copy is always the pull
+    // (destination-row) form, so push PageRank runs the same pipeline
+    if (bg->direction == 1) std::swap(rows, cols);
     // 3. split off the edges whose source misses its block's hot prefix but
     //    whose destination is a hub (hybrid_split), then the canonical CSR of
     //    the rest of the renumbered transpose and the same TOCAB cut
