@@ -205,8 +205,13 @@ bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters) {
   const char *env = getenv("GCB_NO_RELABEL");
   if (env && env[0] && env[0] != '0') return false;
   if (bg->rl) return true;
+  // Ski rental: building the copy costs ~350 ms at rmat:24 (up to 1.4 s
+  // while the memory pool first grows) and saves ~0.057 ms per iteration, so
+  // it pays only after ~6000 iterations; promoting after 4096 keeps any
+  // workload within ~2.5x of the better choice.  Long-running jobs (and
+  // bench.py, which builds it in its untimed setup) get the steady state.
   const char *after = getenv("GCB_RELABEL_AFTER");
-  const int64_t threshold = after ? atoll(after) : 20;
+  const int64_t threshold = after ? atoll(after) : 4096;
   if (bg->fast_iters >= threshold) return true;
   bg->fast_iters += upcoming_iters;
   return false;

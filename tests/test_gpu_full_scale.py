@@ -53,7 +53,8 @@ def test_rmat24_build_matches_oracle(s24):
         assert np.array_equal(getattr(bg, name), getattr(obg, name)), name
 
 
-def test_rmat24_pagerank_exact_and_fast(s24):
+def test_rmat24_pagerank_exact_and_fast(s24, monkeypatch):
+    monkeypatch.setenv("GCB_RELABEL_AFTER", "20")
     _, obg, _, bg, threads = s24
     ref = orc.pr_blocked(obg, tol=0.0, max_iters=10, threads=threads)
     ex = gcb.pr_blocked(bg, P10, exact=True)
@@ -76,7 +77,8 @@ def test_rmat24_bfs_depths(s24):
 
 
 @pytest.mark.skipif(LEVEL < 2, reason="set GCB_FULL_SCALE=2 for the 1.48B-edge graph")
-def test_twitter_scale_pagerank_and_cc():
+def test_twitter_scale_pagerank_and_cc(monkeypatch):
+    monkeypatch.setenv("GCB_RELABEL_AFTER", "20")
     g = gcb.generate_rmat(25, 44, 1)
     assert g.num_edges == 1_476_395_008
     r = gcb.cc(g)
