@@ -199,6 +199,8 @@ struct gcb_blocked {
                                      // from cold sources into hot destinations (owned)
   gcb::DArray<uint32_t> rl_perm;     // [n] original id -> renumbered id
   gcb_blocked *pending_hybrid = nullptr;  // build scratch of ensure_relabeled (owned)
+  gcb_blocked *exact_pull = nullptr;      // push graphs: single-block pull blocking of the
+                                          // transpose for the exact push (relabel.cu, owned)
 
   // ---- tol > 0 PageRank: the convergence loop as one CUDA graph (pr.cu) ----
   struct PrGraph *pr_graph = nullptr;  // owned
@@ -324,6 +326,7 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
 // relabel.cu: degree-ordered execution copy of a pull graph
 bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters);
 gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg);
+gcb_blocked *ensure_exact_pull(gcb_ctx *ctx, gcb_blocked *bg);
 void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, double *y);
 int64_t hot_capacity(gcb_ctx *ctx);    // gather.cu: pull hot-table slots
 int64_t push_hot_slots(gcb_ctx *ctx);  // pr.cu: push hub-accumulator slots

@@ -316,6 +316,7 @@ gcb_blocked::~gcb_blocked() {
   delete rl;
   delete hybrid;
   delete pending_hybrid;
+  delete exact_pull;
   gcb::destroy_pr_graph(pr_graph);
 }
 

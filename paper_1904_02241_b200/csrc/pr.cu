@@ -844,6 +844,12 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
   ensure_derived(ctx, bg);
   if (!(flags & GCB_FLAG_EXACT)) ensure_push_exec(ctx, bg, push_hot_slots(ctx));
   const bool wgt = use_weights && bg->weighted;
+  if ((flags & GCB_FLAG_EXACT) && block_only < 0 && bg->m > 0) {
+    // bincount order == exact pull of the transpose (relabel.cu ensure_exact_pull)
+    gcb_blocked *tp = ensure_exact_pull(ctx, bg);
+    pull_sums(ctx, tp, vals, nullptr, use_weights, flags, -1, sums, true);
+    return;
+  }
   if (flags & GCB_FLAG_EXACT) {
     if (bg->B == 0) return;
     unsigned g = block_only >= 0 ? 1 : grid_for(bg->B, 64, 1 << 20);

@@ -8,8 +8,8 @@ rmat:24:16:1 transpose and TOCAB blocking on the CPU, and the device build must
 match it byte for byte; exact-mode PageRank (10 iterations) must equal the
 oracle's ranks bitwise, and the default fast pipeline (degree-ordered copy,
 hot tables, hybrid push edges) must stay within the north star's 1e-6
-relative tolerance of them.  BFS depths from the hub are compared with the
-oracle's.  Level 2 adds the Twitter-scale graph of configs[4] (1.48 billion
+relative tolerance of them.  BFS depths from the hub and exact push
+PageRank (bincount order) are compared with the oracle's.  Level 2 adds the Twitter-scale graph of configs[4] (1.48 billion
 edges), where the CPU build is too slow to repeat: fast vs exact PageRank on
 the device and the CC label invariants.
 """
@@ -66,14 +66,19 @@ def test_rmat24_pagerank_exact_and_fast(s24, monkeypatch):
         assert rel_err(fast.ranks, ref.ranks) <= TOL
 
 
-def test_rmat24_bfs_depths(s24):
-    ogt, _, gt, bg, _ = s24
+def test_rmat24_bfs_depths_and_exact_push(s24):
+    ogt, _, gt, bg, threads = s24
     og = orc.transpose(ogt)
     g = gcb.transpose(gt)
     want, _ = orc.bfs_depth(og, 0)
     got = gcb.bfs(g, 0, g_blocked=bg)
     assert np.array_equal(got.depth, want)
     assert "blocked-pull" in got.directions  # the TOCAB pull side ran
+    # push PageRank in the reference's bincount order, bit for bit
+    ref = orc.pr_blocked(orc.partition_tocab(og, "push", 1 << 23), tol=0.0, max_iters=10,
+                         threads=threads)
+    ex = gcb.pr_blocked(gcb.partition_tocab(g, "push", 1 << 23), P10, exact=True)
+    assert np.array_equal(ex.ranks, ref.ranks)
 
 
 @pytest.mark.skipif(LEVEL < 2, reason="set GCB_FULL_SCALE=2 for the 1.48B-edge graph")
