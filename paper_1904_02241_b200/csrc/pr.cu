@@ -1249,8 +1249,15 @@ int gcb_process_block_push(gcb_ctx *ctx, gcb_blocked *bg, int64_t block, const d
   h2d(ctx, bg->contrib.p, contrib_host, n);
   h2d(ctx, dsums.p, sums_host, n);
   GCB_CUDA(cudaMemsetAsync(local.p, 0, (n ? n : 1) * sizeof(double), ctx->stream));
-  // unweighted, like the reference (kernels.py:291-293)
-  push_scatter(ctx, bg, bg->contrib.p, local.p, false, flags, block);
+  // unweighted, like the reference (kernels.py:291-293).  Exact: the block's
+  // destinations [lo, hi) get exactly their bincount sums from the exact pull
+  // over the transpose (every destination lives in one push block); the rows
+  // of other blocks land in `local` too but are not added below.
+  if ((flags & GCB_FLAG_EXACT) && bg->m > 0)
+    pull_sums(ctx, ensure_exact_pull(ctx, bg), bg->contrib.p, nullptr, false, flags, -1, local.p,
+              true);
+  else
+    push_scatter(ctx, bg, bg->contrib.p, local.p, false, flags, block);
   const int64_t lo = block * bg->width, hi = (lo + bg->width < n) ? lo + bg->width : n;
   if (hi > lo) {
     k_add_range<<<grid_for(hi - lo, 256, 4096), 256, 0, ctx->stream>>>(lo, hi, local.p, dsums.p);
