@@ -836,7 +836,8 @@ __device__ __forceinline__ double bc_term(double sv, double sw, double dw) {
   return __dmul_rn(__ddiv_rn(sv, sw), __dadd_rn(1.0, dw));
 }
 
-// thread per vertex of the level, sequential in CSR order (exact)
+// thread per vertex of the level, sequential in CSR order (exact); vertices
+// with more than kExactShort out-edges are k_bc_back_exact_long's
 __global__ void k_bc_back_exact(int64_t cnt, const uint32_t *__restrict__ verts, int32_t level,
                                 const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
                                 const int32_t *__restrict__ depth, const double *__restrict__ sigma,
@@ -844,6 +845,7 @@ __global__ void k_bc_back_exact(int64_t cnt, const uint32_t *__restrict__ verts,
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t v = verts[i];
+    if (ro[v + 1] - ro[v] > (int64_t)kExactShort) continue;
     const double sv = sigma[v];
     double acc = 0.0;
     for (int64_t e = ro[v]; e < ro[v + 1]; ++e) {
@@ -851,6 +853,83 @@ __global__ void k_bc_back_exact(int64_t cnt, const uint32_t *__restrict__ verts,
       if (depth[w] == level + 1) acc = __dadd_rn(acc, bc_term(sv, sigma[w], delta[w]));
     }
     delta[v] = __dadd_rn(delta[v], acc);
+  }
+}
+
+// Exact dependency sum of a vertex with many out-edges (a hub took ~100 ms on
+// one thread, a dependent round trip per edge).  A warp per such vertex: the
+// lanes load steps of 256 edges (8 each), software-pipelined -- column ids two
+// steps ahead, depth/sigma/delta of the successors one step ahead -- turn them
+// into terms (a non-successor's term is +0.0, which leaves the non-negative
+// sum unchanged bit for bit), stage them in the warp's shared-memory slot,
+// and the chain adds them in CSR order, as the reference loop does.
+__global__ void k_bc_back_exact_long(int64_t cnt, const uint32_t *__restrict__ verts,
+                                     int32_t level, const int64_t *__restrict__ ro,
+                                     const uint32_t *__restrict__ col,
+                                     const int32_t *__restrict__ depth,
+                                     const double *__restrict__ sigma,
+                                     double *__restrict__ delta) {
+  __shared__ double s_buf[8][256];  // 256-thread CTAs: one slot per warp
+  double *buf = s_buf[threadIdx.x >> 5];
+  constexpr uint32_t kNone = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < cnt; i += nw) {
+    const uint32_t v = verts[i];
+    const int64_t e0 = ro[v], e1 = ro[v + 1];
+    if (e1 - e0 <= (int64_t)kExactShort) continue;
+    const double sv = sigma[v];
+    auto load_cols = [&](int64_t base, uint32_t (&c)[8]) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t e = base + q * 32 + lane;
+        c[q] = e < e1 ? col[e] : kNone;
+      }
+    };
+    auto load_succ = [&](const uint32_t (&c)[8], int (&d)[8], double (&sw)[8], double (&dw)[8]) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        d[q] = -1;
+        if (c[q] != kNone) {
+          d[q] = depth[c[q]];
+          sw[q] = sigma[c[q]];
+          dw[q] = delta[c[q]];
+        }
+      }
+    };
+    uint32_t c1[8], c2[8];
+    int d0[8], d1[8];
+    double s0[8], s1[8], w0[8], w1[8];
+    load_cols(e0, c1);
+    load_succ(c1, d0, s0, w0);  // step 0
+    load_cols(e0 + 256, c1);    // step 1's columns
+    double acc = 0.0;
+    for (int64_t base = e0; base < e1; base += 256) {
+      if (base + 256 < e1) {
+        load_succ(c1, d1, s1, w1);  // step s+1
+        load_cols(base + 512, c2);  // step s+2
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        buf[q * 32 + lane] = d0[q] == level + 1 ? bc_term(sv, s0[q], w0[q]) : 0.0;
+      __syncwarp();
+      const int n = (int)(e1 - base < 256 ? e1 - base : 256);
+      if (n == 256) {
+#pragma unroll 64
+        for (int k = 0; k < 256; ++k) acc = __dadd_rn(acc, buf[k]);
+      } else {
+        for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, buf[k]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        d0[q] = d1[q];
+        s0[q] = s1[q];
+        w0[q] = w1[q];
+        c1[q] = c2[q];
+      }
+    }
+    if (lane == 0) delta[v] = __dadd_rn(delta[v], acc);
   }
 }
 
@@ -943,10 +1022,18 @@ static void bc_backward_dev(gcb_ctx *ctx, const gcb_csr *g, const int32_t *depth
   for (int64_t l = L - 2; l >= 0; --l) {
     const int64_t cnt = off[l + 1] - off[l];
     if (!cnt) continue;
-    if (exact) {
+    // the exact kernels (thread per short vertex, pipelined warp per long one)
+    // also beat the warp-per-vertex fast form (rmat:24, 4 sources: 23 ms
+    // against 31 ms for the whole bc), so GCB_BC_WARP=1 alone selects the latter
+    const char *wenv = getenv("GCB_BC_WARP");
+    if (exact || !(wenv && wenv[0] == '1')) {
       k_bc_back_exact<<<grid_for(cnt, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
           cnt, levels + off[l], (int32_t)l, g->ro.p, g->col.p, depth, sigma, delta);
       after_launch(ctx, "k_bc_back_exact");
+      k_bc_back_exact_long<<<grid_for(cnt * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0,
+                             ctx->stream>>>(cnt, levels + off[l], (int32_t)l, g->ro.p, g->col.p,
+                                            depth, sigma, delta);
+      after_launch(ctx, "k_bc_back_exact_long");
     } else {
       k_bc_back_warp<<<grid_for(cnt * 32, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
           cnt, levels + off[l], (int32_t)l, g->ro.p, g->col.p, depth, sigma, delta);
