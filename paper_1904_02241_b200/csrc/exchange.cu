@@ -62,14 +62,10 @@ __global__ void __launch_bounds__(512, 2)
       const uint32_t any = (nm | (nm >> 8) | (nm >> 16) | (nm >> 24)) & 0xffu;
       for (int p = 0; p < P; ++p) {
         if (!((any >> p) & 1u)) continue;
-        double *dst = out[p] + v0 + 4 * i;
-        if (((nm >> p) & 0x01010101u) == 0x01010101u) {
-          st_f64x4(dst, c[0], c[1], c[2], c[3]);  // the whole quad
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if ((nm >> (8 * k + p)) & 1u) dst[k] = c[k];
-        }
+        // the whole 32-byte quad as one full-sector store even when the peer
+        // reads only some of its four entries: the others land on entries the
+        // peer never reads (measured: per-entry 8-byte stores cost more)
+        st_f64x4(out[p] + v0 + 4 * i, c[0], c[1], c[2], c[3]);
       }
     }
   }

@@ -281,8 +281,11 @@ class PeerExchange:
                 need[:cnt] |= (masks[p][v0:v1].to(dev) << p).to(torch.uint8)
         self.need = need
         self.epoch = 0
+        # P2P store bytes per step: a 32-byte quad per (quad, reading peer) pair
         popc = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int64, device=dev)
-        self.bytes_per_step = 8 * int(popc[need[:cnt].long()].sum()) if cnt else 0  # P2P stores
+        q = need.view(-1, 4)
+        quad_or = q[:, 0] | q[:, 1] | q[:, 2] | q[:, 3]
+        self.bytes_per_step = 32 * int(popc[quad_or.long()].sum()) if cnt else 0
 
     def buffer(self, epoch: int) -> int:
         return self._own[epoch % 2]
