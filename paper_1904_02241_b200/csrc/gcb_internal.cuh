@@ -168,6 +168,7 @@ struct gcb_blocked {
   std::vector<int64_t> h_span_base;  // [B+1] prefix of carry-span starts
   gcb::DArray<uint32_t> span_tile;   // tile ids (global) of each row's first carry tile
   gcb::DArray<uint32_t> span_len;    // number of consecutive carry tiles of that row
+  bool long_ready = false;           // long_rows built (ensure_long_rows)
   std::vector<int64_t> h_long_base;  // [B+1] prefix of long rows per block
   gcb::DArray<uint32_t> long_rows;   // local rows with > kExactShort edges (exact pull)
   int64_t R = 0;                     // merge ranges (ceil(n / kMergeK))
@@ -315,6 +316,7 @@ void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out);
 // gather.cu: fast pull gather accumulating into a dense vector (hot staging)
 void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg);
 void ensure_row_bits(gcb_ctx *ctx, gcb_blocked *bg);  // rstart only (tiles.cuh kernels)
+void ensure_long_rows(gcb_ctx *ctx, gcb_blocked *bg);  // exact pull's long-row lists
 void ensure_push_exec(gcb_ctx *ctx, gcb_blocked *bg, int64_t hot_slots);  // push hot destinations
 void gather_accum(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_weights,
                   uint32_t flags, double *out);

@@ -322,6 +322,68 @@ gcb_blocked::~gcb_blocked() {
 
 namespace gcb {
 
+// Long rows per block for the exact pull (a warp each, longest first), built
+// on the first exact pass: the fast paths never read them, and the per-block
+// compaction and sort cost several host round trips per upload.
+void ensure_long_rows(gcb_ctx *ctx, gcb_blocked *bg) {
+  ensure_derived(ctx, bg);
+  if (bg->long_ready) return;
+  const int64_t B = bg->B;
+  {
+    bg->h_long_base.assign(B + 1, 0);
+    std::vector<DArray<uint32_t>> parts;
+    DArray<uint32_t> lflag(bg->L + 1), lpos(bg->L + 1);
+    int64_t total = 0;
+    std::vector<int64_t> cnt(B, 0);
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+      if (Lb == 0) continue;
+      k_long_flags<<<grid_for(Lb, 256, 65536), 256, 0, ctx->stream>>>(Lb, bg->lro.p + rs + b,
+                                                                     kExactShort, lflag.p);
+      after_launch(ctx, "k_long_flags");
+      GCB_CUDA(cudaMemsetAsync(lflag.p + Lb, 0, sizeof(uint32_t), ctx->stream));
+      cub_exclusive_sum_u32(ctx, lflag.p, lpos.p, Lb + 1);
+      uint32_t c = 0;
+      d2h(ctx, &c, lpos.p + Lb, 1);
+      sync(ctx);
+      cnt[b] = c;
+      DArray<uint32_t> part(c ? c : 1);
+      if (c) {
+        k_compact_rows<<<grid_for(Lb, 256, 65536), 256, 0, ctx->stream>>>(Lb, lflag.p, lpos.p, part.p);
+        after_launch(ctx, "k_compact_rows");
+        // longest first: the hub rows' add chains are the kernel's critical
+        // path, so their warps must start at once (rows are independent)
+        DArray<uint32_t> k1(c), k2(c), v2(c);
+        k_row_lengths<<<grid_for(c, 256, 65536), 256, 0, ctx->stream>>>(c, part.p, bg->lro.p + rs + b,
+                                                                       k1.p);
+        after_launch(ctx, "k_row_lengths");
+        uint32_t *rk = nullptr, *rv = nullptr;
+        cub_sort_pairs_desc_u32_u32(ctx, k1.p, k2.p, part.p, v2.p, c, &rk, &rv);
+        if (rv != part.p)
+          GCB_CUDA(cudaMemcpyAsync(part.p, rv, c * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+        sync(ctx);  // k1/k2/v2 are released at scope end
+      }
+      parts.push_back(std::move(part));
+      total += c;
+    }
+    bg->long_rows.alloc(total ? total : 1);
+    int64_t at = 0, pi = 0;
+    for (int64_t b = 0; b < B; ++b) {
+      bg->h_long_base[b] = at;
+      const int64_t Lb = bg->h_row_starts[b + 1] - bg->h_row_starts[b];
+      if (Lb == 0) continue;
+      if (cnt[b])
+        GCB_CUDA(cudaMemcpyAsync(bg->long_rows.p + at, parts[pi].p, cnt[b] * sizeof(uint32_t),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+      at += cnt[b];
+      ++pi;
+    }
+    bg->h_long_base[B] = at;
+    }
+  bg->long_ready = true;
+}
+
 void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
   if (bg->derived) return;
   int64_t n = bg->n, B = bg->B;
@@ -402,59 +464,6 @@ void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
       after_launch(ctx, "k_span_len");
     }
     for (int64_t b = 0; b <= B; ++b) bg->h_span_base[b] = hpos[b];
-  }
-  // long rows per block (exact pull: a warp each)
-  {
-    bg->h_long_base.assign(B + 1, 0);
-    std::vector<DArray<uint32_t>> parts;
-    DArray<uint32_t> lflag(bg->L + 1), lpos(bg->L + 1);
-    int64_t total = 0;
-    std::vector<int64_t> cnt(B, 0);
-    for (int64_t b = 0; b < B; ++b) {
-      const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
-      if (Lb == 0) continue;
-      k_long_flags<<<grid_for(Lb, 256, 65536), 256, 0, ctx->stream>>>(Lb, bg->lro.p + rs + b,
-                                                                     kExactShort, lflag.p);
-      after_launch(ctx, "k_long_flags");
-      GCB_CUDA(cudaMemsetAsync(lflag.p + Lb, 0, sizeof(uint32_t), ctx->stream));
-      cub_exclusive_sum_u32(ctx, lflag.p, lpos.p, Lb + 1);
-      uint32_t c = 0;
-      d2h(ctx, &c, lpos.p + Lb, 1);
-      sync(ctx);
-      cnt[b] = c;
-      DArray<uint32_t> part(c ? c : 1);
-      if (c) {
-        k_compact_rows<<<grid_for(Lb, 256, 65536), 256, 0, ctx->stream>>>(Lb, lflag.p, lpos.p, part.p);
-        after_launch(ctx, "k_compact_rows");
-        // longest first: the hub rows' add chains are the kernel's critical
-        // path, so their warps must start at once (rows are independent)
-        DArray<uint32_t> k1(c), k2(c), v2(c);
-        k_row_lengths<<<grid_for(c, 256, 65536), 256, 0, ctx->stream>>>(c, part.p, bg->lro.p + rs + b,
-                                                                       k1.p);
-        after_launch(ctx, "k_row_lengths");
-        uint32_t *rk = nullptr, *rv = nullptr;
-        cub_sort_pairs_desc_u32_u32(ctx, k1.p, k2.p, part.p, v2.p, c, &rk, &rv);
-        if (rv != part.p)
-          GCB_CUDA(cudaMemcpyAsync(part.p, rv, c * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
-                                   ctx->stream));
-        sync(ctx);  // k1/k2/v2 are released at scope end
-      }
-      parts.push_back(std::move(part));
-      total += c;
-    }
-    bg->long_rows.alloc(total ? total : 1);
-    int64_t at = 0, pi = 0;
-    for (int64_t b = 0; b < B; ++b) {
-      bg->h_long_base[b] = at;
-      const int64_t Lb = bg->h_row_starts[b + 1] - bg->h_row_starts[b];
-      if (Lb == 0) continue;
-      if (cnt[b])
-        GCB_CUDA(cudaMemcpyAsync(bg->long_rows.p + at, parts[pi].p, cnt[b] * sizeof(uint32_t),
-                                 cudaMemcpyDeviceToDevice, ctx->stream));
-      at += cnt[b];
-      ++pi;
-    }
-    bg->h_long_base[B] = at;
   }
   // span tile ids were global; kernels subtract the block's tile base
   // merge bounds

@@ -721,6 +721,7 @@ void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *v
     const uint32_t *idm_b = bg->id_map.p + rs;
     ProfScope ps_gather(ctx, 0);
     if (exact || !(vals || vals32)) {
+      ensure_long_rows(ctx, bg);
       const unsigned g = grid_for(Lb, 256, (int64_t)ctx->num_sms * 16);
       const double *wb = wgt ? bg->w.p + es : nullptr;
       double *o = accum ? out : out + rs;
@@ -783,6 +784,7 @@ void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out);
 // into zeroed sums gives, bit for bit.
 static void exact_pull_concurrent(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool wgt,
                                   double *out) {
+  ensure_long_rows(ctx, bg);
   bg->partials.ensure(bg->L ? bg->L : 1);
   if (!ctx->aux_stream) {
     GCB_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
