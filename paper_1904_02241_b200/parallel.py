@@ -32,7 +32,8 @@ from .graph import CsrGraph
 from .kernels import PrParams, PrResult
 
 __all__ = ["shard_ranges", "DeviceShard", "TorchExchange", "SparseExchange", "PeerExchange",
-           "LoopbackExchange", "ShardedPageRank", "sharded_pagerank_virtual"]
+           "LoopbackExchange", "ShardedPageRank", "ShardedSpmv", "sharded_pagerank_virtual",
+           "sharded_spmv_virtual"]
 
 
 # Cost of one owned vertex relative to one in-edge in a shard's step: the
@@ -497,6 +498,51 @@ class ShardedPageRank:
         if gather_ranks:
             ex.sync_full(ranks)
         return PrResult(ranks, it, conv)
+
+
+class ShardedSpmv:
+    """spmv_blocked (kernels.py:431-487) across destination shards (SURVEY 8e:
+    SpMV shards like PageRank): every rank multiplies its row slab by the full
+    x on its device, rows it does not own come out 0, and the owned slices of
+    y are all-gathered."""
+
+    def __init__(self, engine: DeviceShard, plan: ShardPlan, rank: int, exchange=None):
+        self.engine, self.plan, self.rank = engine, plan, rank
+        self.exchange = exchange if exchange is not None else TorchExchange(plan, rank)
+
+    def run(self, x, gather: bool = True):
+        """x: float64[n] on this rank's device (the full vector).  Returns y,
+        complete when gather, else correct on the owned slice only."""
+        import torch
+
+        eng = self.engine
+        y = torch.zeros(eng.n, dtype=torch.float64, device=eng.device)
+        _lib.check(eng.ctx._lib.gcb_spmv_blocked_dev(
+            eng.ctx.handle, eng.bg.device().raw, ctypes.c_void_p(x.data_ptr()), eng.flags,
+            ctypes.c_void_p(y.data_ptr())), "sharded spmv")
+        if gather:
+            getattr(self.exchange, "sync_full", self.exchange.sync)(y)
+        return y
+
+
+def sharded_spmv_virtual(gt: CsrGraph, x, parts: int, width: int, exact: bool = False) -> np.ndarray:
+    """``parts`` destination shards of y = A x on one GPU: the single-device
+    check of ShardedSpmv (same width as the unsharded blocking: bit-identical
+    in exact mode, since every row keeps its block split and arena order)."""
+    import torch
+
+    plan = ShardPlan(shard_ranges(gt.row_offsets, parts))
+    flags = _lib.FLAG_EXACT if exact else 0
+    shards = [DeviceShard(gt, *plan.owned(r), width, flags) for r in range(parts)]
+    dev = shards[0].device
+    xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+    y = torch.zeros(gt.num_vertices, dtype=torch.float64, device=dev)
+    for r, s in enumerate(shards):
+        a, b = plan.owned(r)
+        yr = ShardedSpmv(s, plan, r, exchange=LoopbackExchange(plan)).run(xd, gather=False)
+        y[a:b] = yr[a:b]
+    torch.cuda.synchronize(dev)
+    return y.cpu().numpy()
 
 
 def sharded_pagerank_virtual(gt: CsrGraph, parts: int, width: int,
