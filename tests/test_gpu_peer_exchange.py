@@ -49,6 +49,9 @@ def _worker(rank, world, port, out_dir):
         results[f"tol_{exact}"] = r.ranks.cpu().numpy()
         results[f"tol_{exact}_it"] = np.array([r.iterations, int(r.converged)])
         ex.close()
+        # sharded SpMV over the same slabs, y all-gathered across the processes
+        x = torch.as_tensor(np.random.default_rng(9).random(gt.num_vertices)).cuda()
+        results[f"spmv_{exact}"] = parallel.ShardedSpmv(eng, plan, rank).run(x).cpu().numpy()
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **results)
     dist.destroy_process_group()
 
@@ -66,6 +69,7 @@ def test_peer_exchange_matches_unsharded(tmp_path, world):
     bg = gcb.partition_tocab(gcb.generate_rmat(scale, ef, seed, transposed=True), "pull", 1 << 12)
     want = gcb.pr_blocked(bg, gcb.PrParams(tol=0.0, max_iters=10), exact=True).ranks
     want_tol = gcb.pr_blocked(bg, gcb.PrParams(tol=1e-9, max_iters=200), exact=True)
+    want_y = gcb.spmv_blocked(bg, np.random.default_rng(9).random(bg.num_vertices), exact=True)
     for rank in range(world):
         got = np.load(tmp_path / f"rank{rank}.npz")
         for rep in range(2):
@@ -75,3 +79,5 @@ def test_peer_exchange_matches_unsharded(tmp_path, world):
         assert (int(it), bool(conv)) == (want_tol.iterations, want_tol.converged)
         assert np.array_equal(got["tol_True"], want_tol.ranks)
         assert np.max(np.abs(got["tol_False"] - want_tol.ranks) / want_tol.ranks) <= 1e-9
+        assert np.array_equal(got["spmv_True"], want_y)
+        assert np.max(np.abs(got["spmv_False"] - want_y) / np.maximum(want_y, 1e-300)) <= 1e-12
