@@ -41,6 +41,15 @@ __global__ void k_tput(int n, const double *in, double *out) {
   if (acc == 12345.0) out[0] = acc;
 }
 
+// the same, but only lane 0 of each warp runs the chain (the other lanes idle)
+__global__ void k_tput_lane0(int n, const double *in, double *out) {
+  if ((threadIdx.x & 31) != 0) return;
+  double acc = 0.0;
+  const double a = in[threadIdx.x & 255];
+  for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, a);
+  if (acc == 12345.0) out[0] = acc;
+}
+
 int main() {
   double *in, *out;
   long long *cyc;
@@ -78,6 +87,15 @@ int main() {
     const double cycles = ms * 1e-3 * clk * 1e3;
     printf("%2d chaining warps per SM: %.3f warp-DADD per SM-cycle (%.1f cycles per add per warp)\n",
            wps, (double)m * wps / cycles, cycles / m);
+    k_tput_lane0<<<ctas, 128>>>(m, in, out);
+    cudaEventRecord(e0);
+    k_tput_lane0<<<ctas, 128>>>(m, in, out);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double c2 = ms * 1e-3 * clk * 1e3;
+    printf("   lane 0 only:            %.3f warp-DADD per SM-cycle (%.1f cycles per add per warp)\n",
+           (double)m * wps / c2, c2 / m);
   }
   return 0;
 }
