@@ -1,7 +1,7 @@
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import paper_1904_02241_b200 as gcb
-for scale in (20, 22):
+for scale in [int(a) for a in sys.argv[1:]] or (20, 22):
     g = gcb.generate_rmat(scale, 16, 1)
     bg = gcb.partition_tocab(g, "push", 1 << (scale - 1))
     for _ in range(2):
