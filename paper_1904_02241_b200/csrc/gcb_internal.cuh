@@ -141,7 +141,8 @@ constexpr int kTileV = 8;              // edges per lane
 constexpr int kTileT = 32 * kTileV;    // edges per warp tile
 constexpr int64_t kColPad = 2 * kTileT; // padding so vector loads never fault
 constexpr int kMergeK = 2048;          // internal merge range width
-constexpr uint32_t kExactShort = 32;    // exact pull: longer rows get a warp each
+constexpr uint32_t kExactShort = 32;    // exact pull: longer rows go to k_pull_exact_long
+constexpr uint32_t kExactMid = 4096;    // ... and rows longer than this get a warp each
 }  // namespace gcb
 
 struct gcb_blocked {
@@ -170,6 +171,7 @@ struct gcb_blocked {
   gcb::DArray<uint32_t> span_len;    // number of consecutive carry tiles of that row
   bool long_ready = false;           // long_rows built (ensure_long_rows)
   std::vector<int64_t> h_long_base;  // [B+1] prefix of long rows per block
+  std::vector<int64_t> h_long_big;   // [B] leading rows longer than kExactMid (a warp each)
   gcb::DArray<uint32_t> long_rows;   // local rows with > kExactShort edges (exact pull)
   int64_t R = 0;                     // merge ranges (ceil(n / kMergeK))
   gcb::DArray<int64_t> bounds;       // [B][R+1] arena positions per range

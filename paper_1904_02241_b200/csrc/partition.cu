@@ -270,6 +270,13 @@ __global__ void k_compact_rows(int64_t Lb, const uint32_t *__restrict__ flag,
     if (flag[r]) out[pos[r]] = (uint32_t)r;
 }
 
+__global__ void k_count_above(int64_t c, const uint32_t *__restrict__ keys, uint32_t thr,
+                              uint32_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (keys[i] > thr) atomicAdd(out, 1u);
+}
+
 __global__ void k_row_lengths(int64_t c, const uint32_t *__restrict__ rows,
                               const uint32_t *__restrict__ lro_b, uint32_t *__restrict__ len) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c;
@@ -331,6 +338,7 @@ void ensure_long_rows(gcb_ctx *ctx, gcb_blocked *bg) {
   const int64_t B = bg->B;
   {
     bg->h_long_base.assign(B + 1, 0);
+    std::vector<int64_t> big(B, 0);
     std::vector<DArray<uint32_t>> parts;
     DArray<uint32_t> lflag(bg->L + 1), lpos(bg->L + 1);
     int64_t total = 0;
@@ -362,7 +370,15 @@ void ensure_long_rows(gcb_ctx *ctx, gcb_blocked *bg) {
         if (rv != part.p)
           GCB_CUDA(cudaMemcpyAsync(part.p, rv, c * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
                                    ctx->stream));
+        // how many lead the list with more than kExactMid edges
+        uint32_t *nbig = rk == k1.p ? k2.p : k1.p;
+        GCB_CUDA(cudaMemsetAsync(nbig, 0, sizeof(uint32_t), ctx->stream));
+        k_count_above<<<grid_for(c, 256, 4096), 256, 0, ctx->stream>>>(c, rk, kExactMid, nbig);
+        after_launch(ctx, "k_count_above");
+        uint32_t hb = 0;
+        d2h(ctx, &hb, nbig, 1);
         sync(ctx);  // k1/k2/v2 are released at scope end
+        big[b] = hb;
       }
       parts.push_back(std::move(part));
       total += c;
@@ -380,7 +396,8 @@ void ensure_long_rows(gcb_ctx *ctx, gcb_blocked *bg) {
       ++pi;
     }
     bg->h_long_base[B] = at;
-    }
+    bg->h_long_big = big;
+  }
   bg->long_ready = true;
 }
 

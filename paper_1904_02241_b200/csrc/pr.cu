@@ -238,17 +238,88 @@ __global__ void k_pull_exact(const uint32_t *__restrict__ col_b, const double *_
   }
 }
 
+// Rows of kExactShort..kExactMid edges, 32 per warp, one per lane: each lane
+// runs its own row's chain, so one warp-DADD serves 32 rows (the FP64 pipe
+// issues ~1.75 warp-DADDs per SM-cycle whatever the active mask), with the
+// lane's column ids two steps and its values one step ahead of its adds.
+// Rows come sorted by length, so a warp's 32 rows are about equally long.
+template <bool WGT, bool ACCUM>
+__device__ __forceinline__ void exact_rows_by_lane(const uint32_t *__restrict__ col_b,
+                                                   const double *__restrict__ w_b,
+                                                   const uint32_t *__restrict__ lro_b,
+                                                   const uint32_t *__restrict__ id_map_b,
+                                                   const uint32_t *__restrict__ rows, int64_t nrows,
+                                                   const double *__restrict__ vals,
+                                                   double *__restrict__ out, int lane) {
+  constexpr int S = 8;
+  const bool act = lane < nrows;
+  const uint32_t i = act ? rows[lane] : 0u;
+  const uint32_t e0 = act ? lro_b[i] : 0u, e1 = act ? lro_b[i + 1] : 0u;
+  const uint32_t steps = (e1 - e0 + S - 1) / S;
+  const uint32_t wsteps = __reduce_max_sync(0xffffffffu, steps);
+  auto load_cols = [&](uint32_t e, uint32_t (&c)[S], double (&w)[S]) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      c[k] = e + k < e1 ? col_b[e + k] : 0xffffffffu;
+      if (WGT) w[k] = e + k < e1 ? w_b[e + k] : 0.0;
+    }
+  };
+  auto load_vals = [&](const uint32_t (&c)[S], const double (&w)[S], double (&x)[S]) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      x[k] = 0.0;
+      if (c[k] != 0xffffffffu) {
+        x[k] = vals[c[k]];
+        if (WGT) x[k] = __dmul_rn(w[k], x[k]);
+      }
+    }
+  };
+  uint32_t c1[S], c2[S];
+  double w1[S], w2[S], x[S], nx[S];
+  load_cols(e0, c1, w1);
+  load_vals(c1, w1, x);
+  load_cols(e0 + S, c1, w1);
+  double acc = 0.0;
+  for (uint32_t st = 0; st < wsteps; ++st) {
+    const uint32_t e = e0 + st * S;
+    load_vals(c1, w1, nx);
+    load_cols(e + 2 * S, c2, w2);
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+      if (e + k < e1) acc = __dadd_rn(acc, x[k]);
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      x[k] = nx[k];
+      c1[k] = c2[k];
+      if (WGT) w1[k] = w2[k];
+    }
+  }
+  if (act) exact_store<WGT, ACCUM>(out, id_map_b, i, acc);
+}
+
+// Rows longer than kExactShort.  The first nbig rows of the (longest-first)
+// list, longer than kExactMid, get a warp each; the rest go 32 per warp,
+// one per lane (exact_rows_by_lane).  Work items: the big rows first, then
+// the 32-row groups, over a grid-stride of warps.
 template <bool WGT, bool ACCUM>
 __global__ void k_pull_exact_long(const uint32_t *__restrict__ col_b, const double *__restrict__ w_b,
                                   const uint32_t *__restrict__ lro_b,
                                   const uint32_t *__restrict__ id_map_b,
                                   const uint32_t *__restrict__ long_rows, int64_t nlong,
-                                  const double *__restrict__ vals, double *__restrict__ out) {
+                                  int64_t nbig, const double *__restrict__ vals,
+                                  double *__restrict__ out) {
   __shared__ double s_buf[8][256];  // one 256-value slot per warp (256-thread CTAs)
   double *buf = s_buf[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nlong; j += nw) {
+  const int64_t items = nbig + (nlong - nbig + 31) / 32;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < items; j += nw) {
+    if (j >= nbig) {
+      const int64_t first = nbig + (j - nbig) * 32;
+      exact_rows_by_lane<WGT, ACCUM>(col_b, w_b, lro_b, id_map_b, long_rows + first,
+                                     nlong - first, vals, out, lane);
+      continue;
+    }
     const uint32_t i = long_rows[j];
     const uint32_t b0 = lro_b[i], b1 = lro_b[i + 1];
     double acc = 0.0;
@@ -727,19 +798,20 @@ void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *v
       double *o = accum ? out : out + rs;
       const uint32_t *lr = bg->long_rows.p + bg->h_long_base[b];
       const int64_t nl = bg->h_long_base[b + 1] - bg->h_long_base[b];
-      const unsigned gl = grid_for(nl * 32, 256, (int64_t)ctx->num_sms * 16);
+      const int64_t nb = bg->h_long_big[b];
+      const unsigned gl = grid_for((nb + (nl - nb + 31) / 32) * 32, 256, (int64_t)ctx->num_sms * 16);
       if (wgt && accum) {
         k_pull_exact<true, true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
-        if (nl) k_pull_exact_long<true, true><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+        if (nl) k_pull_exact_long<true, true><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, nb, vals, o);
       } else if (wgt) {
         k_pull_exact<true, false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
-        if (nl) k_pull_exact_long<true, false><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+        if (nl) k_pull_exact_long<true, false><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, nb, vals, o);
       } else if (accum) {
         k_pull_exact<false, true><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
-        if (nl) k_pull_exact_long<false, true><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+        if (nl) k_pull_exact_long<false, true><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, nb, vals, o);
       } else {
         k_pull_exact<false, false><<<g, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
-        if (nl) k_pull_exact_long<false, false><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+        if (nl) k_pull_exact_long<false, false><<<gl, 256, 0, ctx->stream>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, nb, vals, o);
       }
       after_launch(ctx, "k_pull_exact");
       continue;
@@ -804,14 +876,15 @@ static void exact_pull_concurrent(gcb_ctx *ctx, gcb_blocked *bg, const double *v
     double *o = bg->partials.p + rs;
     const uint32_t *lr = bg->long_rows.p + bg->h_long_base[b];
     const int64_t nl = bg->h_long_base[b + 1] - bg->h_long_base[b];
+    const int64_t nb = bg->h_long_big[b];
     const unsigned g = grid_for(Lb, 256, (int64_t)ctx->num_sms * 16);
-    const unsigned gl = grid_for(nl * 32, 256, (int64_t)ctx->num_sms * 16);
+    const unsigned gl = grid_for((nb + (nl - nb + 31) / 32) * 32, 256, (int64_t)ctx->num_sms * 16);
     if (wgt) {
       k_pull_exact<true, false><<<g, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
-      if (nl) k_pull_exact_long<true, false><<<gl, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+      if (nl) k_pull_exact_long<true, false><<<gl, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, nb, vals, o);
     } else {
       k_pull_exact<false, false><<<g, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
-      if (nl) k_pull_exact_long<false, false><<<gl, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, vals, o);
+      if (nl) k_pull_exact_long<false, false><<<gl, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, nb, vals, o);
     }
     after_launch(ctx, "k_pull_exact");
   }
