@@ -684,28 +684,6 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
-template <bool WGT>
-__global__ void k_push_exact(int64_t B, const int64_t *__restrict__ row_starts,
-                             const int64_t *__restrict__ edge_starts,
-                             const uint32_t *__restrict__ lro, const uint32_t *__restrict__ id_map,
-                             const uint32_t *__restrict__ col, const double *__restrict__ w,
-                             const double *__restrict__ vals, double *__restrict__ sums,
-                             int64_t only) {
-  const int64_t b = (only >= 0) ? only : (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B || (only >= 0 && (blockIdx.x | threadIdx.x))) return;
-  const int64_t rs = row_starts[b], re = row_starts[b + 1], es = edge_starts[b];
-  const uint32_t *lro_b = lro + rs + b;
-  for (int64_t i = 0; i < re - rs; ++i) {
-    const double x = vals[id_map[rs + i]];
-    for (uint32_t e = lro_b[i]; e < lro_b[i + 1]; ++e) {
-      double y = x;
-      if (WGT) y = __dmul_rn(w[es + e], x);
-      const uint32_t d = col[es + e];
-      sums[d] = __dadd_rn(sums[d], y);
-    }
-  }
-}
-
 __global__ void k_add_range(int64_t lo, int64_t hi, const double *__restrict__ local,
                             double *__restrict__ sums) {
   for (int64_t v = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < hi;
@@ -919,25 +897,12 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
   ensure_derived(ctx, bg);
   if (!(flags & GCB_FLAG_EXACT)) ensure_push_exec(ctx, bg, push_hot_slots(ctx));
   const bool wgt = use_weights && bg->weighted;
-  if ((flags & GCB_FLAG_EXACT) && block_only < 0 && bg->m > 0) {
-    // bincount order == exact pull of the transpose (relabel.cu ensure_exact_pull)
-    gcb_blocked *tp = ensure_exact_pull(ctx, bg);
-    pull_sums(ctx, tp, vals, nullptr, use_weights, flags, -1, sums, true);
-    return;
-  }
   if (flags & GCB_FLAG_EXACT) {
-    if (bg->B == 0) return;
-    unsigned g = block_only >= 0 ? 1 : grid_for(bg->B, 64, 1 << 20);
-    unsigned t = block_only >= 0 ? 1 : 64;
-    if (wgt)
-      k_push_exact<true><<<g, t, 0, ctx->stream>>>(bg->B, bg->row_starts.p, bg->edge_starts.p,
-                                                    bg->lro.p, bg->id_map.p, bg->col.p, bg->w.p,
-                                                    vals, sums, block_only);
-    else
-      k_push_exact<false><<<g, t, 0, ctx->stream>>>(bg->B, bg->row_starts.p, bg->edge_starts.p,
-                                                     bg->lro.p, bg->id_map.p, bg->col.p, nullptr,
-                                                     vals, sums, block_only);
-    after_launch(ctx, "k_push_exact");
+    // bincount order == exact pull of the transpose (relabel.cu ensure_exact_pull);
+    // per-block exact scatters go through gcb_process_block_push
+    GCB_REQUIRE(block_only < 0, "exact push_scatter covers whole graphs");
+    if (bg->m == 0) return;
+    pull_sums(ctx, ensure_exact_pull(ctx, bg), vals, nullptr, use_weights, flags, -1, sums, true);
     return;
   }
   for (int64_t b = 0; b < bg->B; ++b) {
