@@ -933,6 +933,73 @@ __global__ void k_bc_back_exact_long(int64_t cnt, const uint32_t *__restrict__ v
   }
 }
 
+// fast mode, long vertices: a CTA per vertex (from the level's compacted
+// list of long vertices), each thread sums a strided share of the edges with
+// 4 gathers in flight, then a block reduction -- no add chain, so a hub's
+// 370K out-edges no longer set the pass's critical path
+__global__ void k_bc_long_flags(int64_t cnt, const uint32_t *__restrict__ verts,
+                                const int64_t *__restrict__ ro, uint32_t *__restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = verts[i];
+    flag[i] = ro[v + 1] - ro[v] > (int64_t)kExactShort ? 1u : 0u;
+  }
+}
+
+__global__ void k_bc_compact(int64_t cnt, const uint32_t *__restrict__ verts,
+                             const uint32_t *__restrict__ flag, const uint32_t *__restrict__ pos,
+                             uint32_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (flag[i]) out[pos[i]] = verts[i];
+}
+
+__global__ void __launch_bounds__(256)
+    k_bc_back_cta(int64_t nlong, const uint32_t *__restrict__ longv, int32_t level,
+                  const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
+                  const int32_t *__restrict__ depth, const double *__restrict__ sigma,
+                  double *__restrict__ delta) {
+  __shared__ double red[8];
+  for (int64_t j = blockIdx.x; j < nlong; j += gridDim.x) {
+    const uint32_t v = longv[j];
+    const int64_t e0 = ro[v], e1 = ro[v + 1];
+    const double sv = sigma[v];
+    double acc = 0.0;
+    int64_t e = e0 + threadIdx.x;
+    for (; e + 3 * 256 < e1; e += 4 * 256) {
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[k] = col[e + k * 256];
+      int d[4];
+      double sw[4], dw[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        d[k] = depth[w[k]];
+        sw[k] = sigma[w[k]];
+        dw[k] = delta[w[k]];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (d[k] == level + 1) acc += bc_term(sv, sw[k], dw[k]);
+    }
+    for (; e < e1; e += 256) {
+      const uint32_t w = col[e];
+      if (depth[w] == level + 1) acc += bc_term(sv, sigma[w], delta[w]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += red[k];
+      delta[v] = delta[v] + t;
+    }
+    __syncthreads();
+  }
+}
+
 // warp per vertex of the level (fast)
 __global__ void k_bc_back_warp(int64_t cnt, const uint32_t *__restrict__ verts, int32_t level,
                                const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
@@ -1019,14 +1086,41 @@ static void bc_backward_dev(gcb_ctx *ctx, const gcb_csr *g, const int32_t *depth
                             const double *sigma, const uint32_t *levels,
                             const std::vector<int64_t> &off, bool exact, double *delta) {
   const int64_t L = (int64_t)off.size() - 1;  // number of non-empty levels
+  DArray<uint32_t> flag, pos, longv;  // fast mode: the level's long vertices
   for (int64_t l = L - 2; l >= 0; --l) {
     const int64_t cnt = off[l + 1] - off[l];
     if (!cnt) continue;
-    // the exact kernels (thread per short vertex, pipelined warp per long one)
-    // also beat the warp-per-vertex fast form (rmat:24, 4 sources: 23 ms
-    // against 31 ms for the whole bc), so GCB_BC_WARP=1 alone selects the latter
+    // fast: short vertices a thread each, long ones a CTA each (16 ms for 4
+    // sources at rmat:24); exact: the order-keeping kernels (23 ms); the older
+    // warp-per-vertex fast form (31 ms) stays behind GCB_BC_WARP=1
     const char *wenv = getenv("GCB_BC_WARP");
-    if (exact || !(wenv && wenv[0] == '1')) {
+    if (!exact && !(wenv && wenv[0] == '1')) {
+      // fast: thread per short vertex, a CTA per long one
+      k_bc_back_exact<<<grid_for(cnt, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          cnt, levels + off[l], (int32_t)l, g->ro.p, g->col.p, depth, sigma, delta);
+      after_launch(ctx, "k_bc_back_exact");
+      flag.ensure(cnt + 1);
+      pos.ensure(cnt + 1);
+      longv.ensure(cnt);
+      k_bc_long_flags<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(cnt, levels + off[l],
+                                                                         g->ro.p, flag.p);
+      after_launch(ctx, "k_bc_long_flags");
+      GCB_CUDA(cudaMemsetAsync(flag.p + cnt, 0, sizeof(uint32_t), ctx->stream));
+      cub_exclusive_sum_u32(ctx, flag.p, pos.p, cnt + 1);
+      uint32_t *hn = (uint32_t *)ctx->pinned;
+      d2h(ctx, hn, pos.p + cnt, 1);
+      sync(ctx);
+      const int64_t nl = *hn;
+      if (nl) {
+        k_bc_compact<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(cnt, levels + off[l],
+                                                                         flag.p, pos.p, longv.p);
+        after_launch(ctx, "k_bc_compact");
+        k_bc_back_cta<<<(unsigned)std::min<int64_t>(nl, (int64_t)ctx->num_sms * 8), 256, 0,
+                        ctx->stream>>>(nl, longv.p, (int32_t)l, g->ro.p, g->col.p, depth, sigma,
+                                       delta);
+        after_launch(ctx, "k_bc_back_cta");
+      }
+    } else if (exact || !(wenv && wenv[0] == '1')) {
       k_bc_back_exact<<<grid_for(cnt, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
           cnt, levels + off[l], (int32_t)l, g->ro.p, g->col.p, depth, sigma, delta);
       after_launch(ctx, "k_bc_back_exact");
