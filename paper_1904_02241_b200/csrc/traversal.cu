@@ -485,11 +485,24 @@ __global__ void k_cc_flatten(int64_t n, uint32_t *parent) {
 // every edge (u, v), edge-balanced (a hub row no longer serialises on one
 // warp); after the sampling rounds most endpoints already point straight at
 // the giant root, so the common case is two reads and no atomics
+// src[e] = source row of edge e.  A warp takes 32 consecutive rows: one
+// coalesced load of their 33 offsets (the row-per-warp form waited out two
+// dependent offset loads per row: 1.0 ms at rmat:24), then the rows' runs are
+// written in turn, the lanes striding over each run.
 __global__ void k_cc_src(int64_t n, const int64_t *__restrict__ ro, uint32_t *__restrict__ src) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nw)
-    for (int64_t k = ro[u] + lane; k < ro[u + 1]; k += 32) src[k] = (uint32_t)u;
+  for (int64_t u0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; u0 < n;
+       u0 += nw * 32) {
+    const int64_t my = u0 + lane <= n ? ro[u0 + lane] : 0;
+    const int64_t last = u0 + 32 <= n ? ro[u0 + 32] : ro[n];
+    const int rows = (int)(n - u0 < 32 ? n - u0 : 32);
+    for (int r = 0; r < rows; ++r) {
+      const int64_t s = __shfl_sync(0xffffffffu, my, r);
+      const int64_t e = r + 1 < 32 ? __shfl_sync(0xffffffffu, my, r + 1) : last;
+      for (int64_t k = s + lane; k < e; k += 32) src[k] = (uint32_t)(u0 + r);
+    }
+  }
 }
 
 __global__ void k_cc_edges(int64_t m, const uint32_t *__restrict__ src,
@@ -668,7 +681,7 @@ int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_c
       after_launch(ctx, "k_cc_flatten");
     }
     DArray<uint32_t> src(g->m);
-    k_cc_src<<<grid_for(n * 32, 256, 65536), 256, 0, ctx->stream>>>(n, g->ro.p, src.p);
+    k_cc_src<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, g->ro.p, src.p);
     after_launch(ctx, "k_cc_src");
     k_cc_edges<<<grid_for(g->m, 256, (int64_t)ctx->num_sms * 32), 256, 0, ctx->stream>>>(
         g->m, src.p, g->col.p, parent.p);
