@@ -109,6 +109,16 @@ static int hybrid_mode() {
 
 bool hybrid_enabled() { return hybrid_mode() != 0; }
 
+// Hub destinations of the hybrid class (and slots of its push table): 20480
+// ran the iteration 0.7% faster than the full 24576-slot table at rmat:24
+// (gather 0.791 vs 0.796 ms, three runs each); GCB_HYBRID_HUBS overrides.
+static int64_t hybrid_hub_slots(gcb_ctx *ctx) {
+  const char *env = getenv("GCB_HYBRID_HUBS");
+  const int64_t want = env ? atoll(env) : 20480;
+  const int64_t cap = push_hot_slots(ctx);
+  return want < cap ? want : cap;
+}
+
 // The push pass has a fixed cost -- its own launch, and every CTA flushes its
 // hub table (num_sms x slots global adds) -- against a per-edge saving over the
 // pull gather.  Fitted on rmat:21/22/24/25:44 (ms per iteration, hybrid minus
@@ -170,7 +180,7 @@ int64_t hybrid_split(gcb_ctx *ctx, gcb_blocked *bg, DArray<uint32_t> &rows, DArr
   const int64_t n = bg->n, m = bg->m;
   *push_csr = nullptr;
   const int64_t hs = hot_capacity(ctx);
-  const int64_t hd = push_hot_slots(ctx);
+  const int64_t hd = hybrid_hub_slots(ctx);
   if (hs <= 0 || hd <= 0 || bg->width <= hs) return m;  // whole slices are hot already
   DArray<uint8_t> hot_dst(n);
   {
@@ -336,6 +346,7 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
     rl->is_relabeled = true;
     if (bg->pending_hybrid) {
       rl->hybrid = bg->pending_hybrid;
+      ensure_push_exec(ctx, rl->hybrid, hybrid_hub_slots(ctx));  // table sized to the hubs
       bg->pending_hybrid = nullptr;
       // the pull copy no longer holds every edge: its out-degrees are the
       // whole graph's, renumbered (kernels.py:324-330)
