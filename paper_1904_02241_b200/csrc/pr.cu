@@ -203,12 +203,13 @@ __global__ void k_fixup(int64_t nspans, const uint32_t *__restrict__ span_tile,
 }
 
 // K2 exact: storage-order sums (kernels.py:155-170), bit-identical.  Rows of
-// up to kExactShort edges: one thread per row.  Longer rows (listed once per
-// block, ensure_derived) get a warp each: the lanes load and (if weighted)
-// multiply 32 edges in parallel, then every lane adds the 32 values in edge
-// order from the shuffles, so the rounding sequence is exactly the
-// sequential one.  (One thread per row left the 370K-edge hub row of rmat:24
-// on a single thread: 28 ms per exact iteration.)
+// up to kExactShort edges: one thread per row (k_pull_exact).  Longer rows
+// (listed per block, longest first, by ensure_long_rows) go to
+// k_pull_exact_long: up to kExactMid edges one row per lane, longer ones a
+// warp each whose lanes gather in parallel while one add chain walks the
+// values in edge order -- every row's rounding sequence is the sequential
+// one.  (One thread per row left the 370K-edge hub row of rmat:24 on a single
+// thread: 28 ms per exact iteration.)
 template <bool WGT, bool ACCUM>
 __device__ __forceinline__ void exact_store(double *out, const uint32_t *id_map_b, int64_t i, double s) {
   if (ACCUM) {
