@@ -276,6 +276,16 @@ int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_c
 int gcb_bc(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, const int64_t *sources_host,
            int64_t num_sources, int mode, int64_t capacity_bytes, int64_t value_bytes,
            uint32_t flags, double *centrality_host);
+/* bc_single_source traversal.py:239-254: forward sweep with path counts and
+ * the dependency pass on the device; delta (delta[source] = 0), the final
+ * depth / sigma, the per-level vertex lists (concatenated, sizes in
+ * level_sizes_host) and the per-expansion directions (1 = blocked pull) */
+int gcb_bc_single_source(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t source,
+                         int mode, int64_t capacity_bytes, int64_t value_bytes, uint32_t flags,
+                         double *delta_host, int32_t *depth_host, double *sigma_host,
+                         uint32_t *level_verts_host, int64_t *level_sizes_host,
+                         uint8_t *directions_host, int64_t max_levels, int64_t *num_levels,
+                         int64_t *num_expansions);
 /* bc_backward traversal.py:212-236 for a given forward state: depth[n]
  * (INT32_MAX = unreached), sigma[n]; writes delta[n] with delta[source] = 0. */
 int gcb_bc_backward(gcb_ctx *ctx, const gcb_csr *g, const int32_t *depth_host,

@@ -103,6 +103,8 @@ SIGNATURES = {
     "gcb_cc": ([c_vp, c_vp, P_u32, P_i64], c_int),
     "gcb_bc": ([c_vp, c_vp, c_vp, P_i64, c_i64, c_int, c_i64, c_i64, c_u32, P_dbl], c_int),
     "gcb_bc_backward": ([c_vp, c_vp, P_i32, P_dbl, c_i64, c_u32, P_dbl], c_int),
+    "gcb_bc_single_source": ([c_vp, c_vp, c_vp, c_i64, c_int, c_i64, c_i64, c_u32, P_dbl, P_i32,
+                              P_dbl, P_u32, P_i64, P_u8, c_i64, P_i64, P_i64], c_int),
 }
 
 _lib = None

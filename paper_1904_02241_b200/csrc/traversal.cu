@@ -1153,7 +1153,7 @@ static void bc_backward_dev(gcb_ctx *ctx, const gcb_csr *g, const int32_t *depth
 static void bc_forward_dev(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int64_t source, int mode,
                            int64_t capacity, int64_t value_bytes, Frontier &F, int32_t *depth,
                            double *sigma, double *sig_add, uint32_t *levels,
-                           std::vector<int64_t> &off) {
+                           std::vector<int64_t> &off, std::vector<uint8_t> *dirs = nullptr) {
   const int64_t n = g->n;
   k_fill_i32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, kInfDepth, depth);
   after_launch(ctx, "k_fill_i32");
@@ -1177,6 +1177,7 @@ static void bc_forward_dev(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int6
     if (mode == GCB_BFS_FORCE_PUSH || !bg) pull = false;
     else if (mode == GCB_BFS_FORCE_PULL) pull = true;
     else pull = (unsigned __int128)work * (unsigned __int128)value_bytes > (unsigned __int128)capacity;
+    if (dirs) dirs->push_back(pull ? 1 : 0);
     if (!pull) {
       if (work) {
         queue_offsets(ctx, g, levels + qoff, qsize, F);
@@ -1284,6 +1285,66 @@ extern "C" int gcb_bc(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, cons
     }
     if (n) d2h(ctx, centrality_host, cent.p, n);
     sync(ctx);
+  } catch (...) {
+    if (owned) gcb_blocked_destroy(owned);
+    throw;
+  }
+  if (owned) gcb_blocked_destroy(owned);
+  GCB_API_END
+}
+
+// bc_single_source (traversal.py:239-254) on the device: the forward sweep with
+// path counts and the dependency pass, results copied back once (the
+// step-by-step form moved depth/sigma across PCIe on every level: 84 ms at
+// rmat:22 from the hub)
+extern "C" int gcb_bc_single_source(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull,
+                                    int64_t source, int mode, int64_t capacity_bytes,
+                                    int64_t value_bytes, uint32_t flags, double *delta_host,
+                                    int32_t *depth_host, double *sigma_host,
+                                    uint32_t *level_verts_host, int64_t *level_sizes_host,
+                                    uint8_t *directions_host, int64_t max_levels,
+                                    int64_t *num_levels, int64_t *num_expansions) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && g && delta_host && depth_host && sigma_host && num_levels && num_expansions,
+              "NULL argument");
+  GCB_REQUIRE(mode >= 0 && mode <= 2, "unknown direction mode");
+  const int64_t n = g->n;
+  GCB_REQUIRE(source >= 0 && source < n, "source %lld out of range", (long long)source);
+  DeviceGuard dg(ctx->device);
+  gcb_blocked *owned = nullptr;
+  gcb_blocked *bg = bg_pull;
+  try {
+    if (mode != GCB_BFS_FORCE_PUSH && !bg) bg = default_pull_blocking(ctx, g, &owned);
+    if (bg) {
+      GCB_REQUIRE(bg->n == n && bg->direction == 0, "g_blocked must be a pull blocking of g");
+      ensure_row_bits(ctx, bg);
+    }
+    DArray<int32_t> depth(n);
+    DArray<double> sigma(n), sig_add(n), delta(n);
+    DArray<uint32_t> levels(n);
+    Frontier F(n);
+    GCB_CUDA(cudaMemsetAsync(F.next.p, 0, F.next.n, ctx->stream));
+    GCB_CUDA(cudaMemsetAsync(sig_add.p, 0, n * sizeof(double), ctx->stream));
+    GCB_CUDA(cudaMemsetAsync(delta.p, 0, n * sizeof(double), ctx->stream));
+    std::vector<int64_t> off;
+    std::vector<uint8_t> dirs;
+    bc_forward_dev(ctx, g, bg, source, mode, capacity_bytes, value_bytes, F, depth.p, sigma.p,
+                   sig_add.p, levels.p, off, &dirs);
+    bc_backward_dev(ctx, g, depth.p, sigma.p, levels.p, off, flags & GCB_FLAG_EXACT, delta.p);
+    const double zero = 0.0;
+    h2d(ctx, delta.p + source, &zero, 1);
+    const int64_t nl = (int64_t)off.size() - 1;
+    d2h(ctx, delta_host, delta.p, n);
+    d2h(ctx, depth_host, depth.p, n);
+    d2h(ctx, sigma_host, sigma.p, n);
+    if (level_verts_host && nl > 0) d2h(ctx, level_verts_host, levels.p, off.back());
+    sync(ctx);
+    *num_levels = nl;
+    *num_expansions = (int64_t)dirs.size();
+    for (int64_t i = 0; i < nl && i < max_levels; ++i)
+      if (level_sizes_host) level_sizes_host[i] = off[i + 1] - off[i];
+    for (int64_t i = 0; i < (int64_t)dirs.size() && i < max_levels; ++i)
+      if (directions_host) directions_host[i] = dirs[i];
   } catch (...) {
     if (owned) gcb_blocked_destroy(owned);
     throw;

@@ -226,9 +226,36 @@ def _forward(g, g_blocked, source, policy, accumulate_sigma):
 def bc_single_source(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
                      policy: DirectionPolicy = DirectionPolicy(), *, exact: bool = True):
     """One source's forward sweep + dependency pass (traversal.py:239-254):
-    returns (delta, state, levels)."""
-    state, levels, _ = _forward(g, g_blocked, int(source), policy, True)
-    delta = bc_backward(g, state.depth, state.sigma, int(source), exact=exact)
+    returns (delta, state, levels).  Both passes run on the device and the
+    results come back once (gcb_bc_single_source); the final state has an
+    empty frontier and level = the number of expansions, as after the
+    reference's loop."""
+    source = int(source)
+    _check_source(g, source)
+    n = g.num_vertices
+    h = g.device()
+    bgh = None
+    if policy.mode != "force-push":
+        if g_blocked is None:
+            g_blocked = partition_tocab(transpose(g), "pull", max(1, n // 8))
+        bgh = g_blocked.device()
+    delta = _lib.host_empty(n, np.float64)
+    depth = _lib.host_empty(n, np.int32)
+    sigma = _lib.host_empty(n, np.float64)
+    verts = _lib.host_empty(n, np.uint32)
+    cap = n + 2
+    sizes = np.zeros(cap, dtype=np.int64)
+    dirs = np.zeros(cap, dtype=np.uint8)
+    nl, ne = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(h.ctx._lib.gcb_bc_single_source(
+        h.ctx.handle, h.raw, None if bgh is None else bgh.raw, source, policy.code,
+        int(policy.cache_capacity_bytes), int(policy.value_bytes),
+        _lib.FLAG_EXACT if exact else 0, _lib.ptr(delta, _lib.P_dbl), _lib.ptr(depth, _lib.P_i32),
+        _lib.ptr(sigma, _lib.P_dbl), _lib.ptr(verts, _lib.P_u32), _lib.ptr(sizes, _lib.P_i64),
+        _lib.ptr(dirs, _lib.P_u8), cap, ctypes.byref(nl), ctypes.byref(ne)), "bc_single_source")
+    bounds = np.concatenate([[0], np.cumsum(sizes[: nl.value])])
+    levels = [verts[bounds[i]:bounds[i + 1]] for i in range(nl.value)]
+    state = TraversalState(depth, sigma, np.zeros(0, dtype=np.uint32), int(ne.value))
     return delta, state, levels
 
 
