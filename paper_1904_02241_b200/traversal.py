@@ -202,27 +202,6 @@ def bc_backward(g: CsrGraph, depth: np.ndarray, sigma: np.ndarray, source: int, 
     return delta
 
 
-def _forward(g, g_blocked, source, policy, accumulate_sigma):
-    """traversal.py:179-198 over the device level steps."""
-    _check_source(g, source)
-    n = g.num_vertices
-    state = TraversalState.initial(n, source)
-    levels = [state.frontier.copy()]
-    directions = []
-    if policy.mode != "force-push" and g_blocked is None:
-        g_blocked = partition_tocab(transpose(g), "pull", max(1, n // 8))
-    while state.frontier.size:
-        step_dir = choose_direction(g, state, policy)
-        directions.append(step_dir)
-        if step_dir == "push":
-            forward_push_step(g, state, accumulate_sigma)
-        else:
-            forward_pull_step(g_blocked, state, accumulate_sigma)
-        if state.frontier.size:
-            levels.append(state.frontier.copy())
-    return state, levels, directions
-
-
 def bc_single_source(g: CsrGraph, source: int, g_blocked: BlockedGraph | None = None,
                      policy: DirectionPolicy = DirectionPolicy(), *, exact: bool = True):
     """One source's forward sweep + dependency pass (traversal.py:239-254):
