@@ -844,10 +844,13 @@ static void exact_pull_concurrent(gcb_ctx *ctx, gcb_blocked *bg, const double *v
   }
   GCB_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
   GCB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->fork_ev, 0));
+  // block 0's long rows (the hub chains, the critical path) start first on the
+  // main stream; every short-row pass and the other blocks run beside them
   for (int64_t b = 0; b < bg->B; ++b) {
     const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
     if (Lb == 0) continue;
     cudaStream_t st = b == 0 ? ctx->stream : ctx->aux_stream;
+    cudaStream_t sst = ctx->aux_stream;
     const int64_t es = bg->h_edge_starts[b];
     const uint32_t *lro_b = bg->lro.p + rs + b;
     const uint32_t *idm_b = bg->id_map.p + rs;
@@ -859,11 +862,11 @@ static void exact_pull_concurrent(gcb_ctx *ctx, gcb_blocked *bg, const double *v
     const unsigned g = grid_for(Lb, 256, (int64_t)ctx->num_sms * 16);
     const unsigned gl = grid_for((nb + (nl - nb + 31) / 32) * 32, 256, (int64_t)ctx->num_sms * 16);
     if (wgt) {
-      k_pull_exact<true, false><<<g, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
       if (nl) k_pull_exact_long<true, false><<<gl, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, nb, vals, o);
+      k_pull_exact<true, false><<<g, 256, 0, sst>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
     } else {
-      k_pull_exact<false, false><<<g, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
       if (nl) k_pull_exact_long<false, false><<<gl, 256, 0, st>>>(bg->col.p + es, wb, lro_b, idm_b, lr, nl, nb, vals, o);
+      k_pull_exact<false, false><<<g, 256, 0, sst>>>(bg->col.p + es, wb, lro_b, idm_b, Lb, vals, o, kExactShort);
     }
     after_launch(ctx, "k_pull_exact");
   }
@@ -1112,7 +1115,7 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   }
   // one iteration's launches (no host synchronisation: also the graph body)
   auto iterate = [&]() {
-    if (!push && exact && !bg->cb && bg->B > 1 && contrib) {
+    if (!push && exact && !bg->cb && bg->B >= 1 && contrib) {
       ProfScope ps(ctx, 0);
       exact_pull_concurrent(ctx, bg, contrib, false, bg->sums.p);
     } else if (!push) {
