@@ -195,8 +195,10 @@ int gcb_pr_shard_step(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, dou
  * init publishes epoch `epoch`; step waits for every peer's epoch - 1,
  * gathers contrib_in (the other buffer), updates the owned slice, stores each
  * contribution into the peers that read it and publishes `epoch`.  Stream-
- * ordered, no host synchronisation; a peer that never publishes makes the
- * wait kernel trap after ~20 s instead of hanging the device. */
+ * ordered, no host synchronisation.  A peer that misses its deadline
+ * (GCB_PEER_TIMEOUT_S, default 120 s) makes the wait kernel record the fact
+ * and return instead of hanging the device; the next step call, or
+ * gcb_peer_check (which synchronises the ctx stream), returns GCB_ECUDA. */
 int gcb_ipc_alloc(gcb_ctx *ctx, int64_t bytes, void **ptr, unsigned char *handle64);
 int gcb_ipc_free(gcb_ctx *ctx, void *ptr);
 int gcb_ipc_open(gcb_ctx *ctx, const unsigned char *handle64, void **ptr);
@@ -205,6 +207,7 @@ int gcb_pr_shard_init_p2p(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1,
                           const uint32_t *deg_dev, double *ranks_dev, double *const *out_dev,
                           const uint8_t *need_dev, int num_ranks, int rank,
                           uint32_t *const *flags_dev, uint32_t epoch);
+int gcb_peer_check(gcb_ctx *ctx);
 int gcb_pr_shard_step_p2p(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, double damping,
                           uint32_t flags, const uint32_t *deg_dev, const double *contrib_in,
                           double *ranks_dev, double *delta_dev, double *const *out_dev,

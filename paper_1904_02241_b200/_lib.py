@@ -72,6 +72,7 @@ SIGNATURES = {
                                c_vp, c_u32], c_int),
     "gcb_pr_shard_step_p2p": ([c_vp, c_vp, c_i64, c_i64, c_dbl, c_u32, c_vp, c_vp, c_vp, c_vp,
                                c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_u32], c_int),
+    "gcb_peer_check": ([c_vp], c_int),
     "gcb_csr_destroy": ([c_vp], c_int),
     "gcb_partition_tocab": ([c_vp, c_vp, c_int, c_i64, PP], c_int),
     "gcb_partition_cb": ([c_vp, c_vp, c_i64, PP], c_int),

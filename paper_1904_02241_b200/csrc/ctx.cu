@@ -124,6 +124,7 @@ int gcb_ctx_destroy(gcb_ctx *ctx) {
   ctx->cub_tmp.release();
   ctx->scratch.release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->peer_err) cudaFreeHost(ctx->peer_err);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);

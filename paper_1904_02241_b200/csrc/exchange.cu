@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "gcb_internal.cuh"
@@ -123,18 +124,47 @@ __global__ void k_signal_peers(uint32_t *const *flags, int P, int self, uint32_t
   f.store(epoch, cuda::memory_order_release);
 }
 
-// wait until every peer q has published epoch >= `epoch` into mine[q]; a peer
-// that never arrives traps after ~20 s instead of hanging the device
-__global__ void k_wait_peers(uint32_t *mine, int P, int self, uint32_t epoch) {
+// wait until every peer q has published epoch >= `epoch` into mine[q].  A
+// peer that misses the deadline (GCB_PEER_TIMEOUT_S, default 120 s) sets
+// *err and the kernel returns: the context stays usable and the host raises
+// at the next step or at gcb_peer_check (a __trap would destroy the context)
+__global__ void k_wait_peers(uint32_t *mine, int P, int self, uint32_t epoch,
+                             uint64_t timeout_ns, volatile unsigned *err) {
   const int q = threadIdx.x;
   if (q >= P || q == self) return;
   cuda::atomic_ref<uint32_t, cuda::thread_scope_system> f(mine[q]);
   uint64_t t0, t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   while ((int32_t)(f.load(cuda::memory_order_acquire) - epoch) < 0) {
+    if (*err) return;  // an earlier wait already gave up
     __nanosleep(200);
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 20000000000ull) __trap();
+    if (t - t0 > timeout_ns) {
+      *err = 1u + (unsigned)q;
+      __threadfence_system();
+      return;
+    }
+  }
+}
+
+static uint64_t peer_timeout_ns() {
+  const char *env = getenv("GCB_PEER_TIMEOUT_S");
+  const double s = env && env[0] ? atof(env) : 120.0;
+  return (uint64_t)((s > 0 ? s : 120.0) * 1e9);
+}
+
+// raise (once) what a previous k_wait_peers recorded
+static void check_peer_error(gcb_ctx *ctx) {
+  if (!ctx->peer_err) {
+    GCB_CUDA(cudaHostAlloc((void **)&ctx->peer_err, sizeof(unsigned), cudaHostAllocMapped));
+    *ctx->peer_err = 0;
+    GCB_CUDA(cudaHostGetDevicePointer((void **)&ctx->peer_err_dev, ctx->peer_err, 0));
+  }
+  const unsigned e = *(volatile unsigned *)ctx->peer_err;
+  if (e) {
+    *(volatile unsigned *)ctx->peer_err = 0;
+    fail(GCB_ECUDA, "peer exchange: rank %u did not publish its epoch within GCB_PEER_TIMEOUT_S "
+                    "(results of the steps since are invalid)", e - 1);
   }
 }
 
@@ -189,6 +219,15 @@ int gcb_ipc_close(gcb_ctx *ctx, void *ptr) {
   GCB_API_END
 }
 
+int gcb_peer_check(gcb_ctx *ctx) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx, "NULL argument");
+  DeviceGuard dg(ctx->device);
+  sync(ctx);
+  check_peer_error(ctx);
+  GCB_API_END
+}
+
 int gcb_pr_shard_init_p2p(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1,
                           const uint32_t *deg_dev, double *ranks_dev, double *const *out_dev,
                           const uint8_t *need_dev, int num_ranks, int rank,
@@ -234,8 +273,10 @@ int gcb_pr_shard_step_p2p(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1,
   const int64_t cnt = v1 - v0;
   const unsigned grid = grid_for((cnt + 3) / 4, 512, (int64_t)(1 << 20) * ctx->num_sms);
   bg->deltas.ensure((int64_t)grid + 2);
+  check_peer_error(ctx);
   // every peer's contributions of the previous epoch have landed
-  k_wait_peers<<<1, 32, 0, ctx->stream>>>(my_flags_dev, num_ranks, rank, epoch - 1);
+  k_wait_peers<<<1, 32, 0, ctx->stream>>>(my_flags_dev, num_ranks, rank, epoch - 1,
+                                          peer_timeout_ns(), ctx->peer_err_dev);
   after_launch(ctx, "k_wait_peers");
   pull_sums(ctx, bg, contrib_in, nullptr, false, flags, -1, bg->sums.p, true);
   if (cnt) {

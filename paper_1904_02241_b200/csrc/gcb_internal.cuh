@@ -109,6 +109,9 @@ struct gcb_ctx {
   cudaStream_t copy_stream = nullptr;  // host->device copies overlapped with kernels
   cudaStream_t aux_stream = nullptr;   // second compute stream (exact pull: blocks 1..B-1)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // peer exchange (exchange.cu): k_wait_peers sets this mapped host word when
+  // a peer misses its deadline, instead of trapping the context
+  unsigned *peer_err = nullptr, *peer_err_dev = nullptr;
   gcb::DArray<uint8_t> cub_tmp;
   gcb::DArray<uint8_t> scratch;  // general scratch
   // optional per-category kernel timing (gcb_ctx_set_profiling)

@@ -403,6 +403,10 @@ void ensure_long_rows(gcb_ctx *ctx, gcb_blocked *bg) {
 
 void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
   if (bg->derived) return;
+  // a captured convergence loop (pr.cu) reads the tables rebuilt below, and
+  // the pool may hand back the same addresses: never replay it afterwards
+  destroy_pr_graph(bg->pr_graph);
+  bg->pr_graph = nullptr;
   int64_t n = bg->n, B = bg->B;
   if (bg->cb) {
     // the CB kernels walk rows directly: out-degrees only

@@ -963,10 +963,11 @@ struct PrGraph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   gcb::DArray<int> state;  // [iterations run, converged, iteration budget]
-  static constexpr int kKey = 16;
+  static constexpr int kKey = 24;
   const void *key[kKey] = {};
   double kd[2] = {0, 0};
   uint32_t kflags = 0;
+  int kdir = -1;
 };
 
 namespace gcb {
@@ -999,7 +1000,8 @@ static bool pr_graph_loop(gcb_ctx *ctx, gcb_blocked *bg, F &&iterate, const void
                           double damping, double tol, uint32_t flags, const double *delta_dev,
                           int budget, int *ran, int *conv) {
   PrGraph *g = bg->pr_graph;
-  bool same = g && g->kd[0] == damping && g->kd[1] == tol && g->kflags == flags;
+  bool same = g && g->kd[0] == damping && g->kd[1] == tol && g->kflags == flags &&
+              g->kdir == bg->direction;
   for (int i = 0; same && i < PrGraph::kKey; ++i) same = g->key[i] == key[i];
   if (!same) {
     destroy_pr_graph(g);
@@ -1055,6 +1057,7 @@ static bool pr_graph_loop(gcb_ctx *ctx, gcb_blocked *bg, F &&iterate, const void
     ng->kd[0] = damping;
     ng->kd[1] = tol;
     ng->kflags = flags;
+    ng->kdir = bg->direction;
     bg->pr_graph = g = ng;
   }
   int *hs = (int *)ctx->pinned;
@@ -1164,7 +1167,12 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
                                           bg->hot_ids.p, bg->rstart.p, bg->tile_row.p,
                                           (const void *)(intptr_t)bg->hot_k,
                                           hy ? hy->xcol.p : nullptr,
-                                          hy ? (const void *)(intptr_t)hy->hot_k : nullptr};
+                                          hy ? (const void *)(intptr_t)hy->hot_k : nullptr,
+                                          // the exact pull's buffers
+                                          bg->partials.p, bg->bounds.p, bg->long_rows.p,
+                                          bg->carry.p, bg->span_tile.p, bg->span_len.p,
+                                          (const void *)(intptr_t)bg->direction,
+                                          (const void *)(intptr_t)bg->B};
         int ran = 0, c2 = 0;
         if (pr_graph_loop(ctx, bg, iterate, key, damping, tol, flags, delta_dev, max_iters - 1,
                           &ran, &c2)) {

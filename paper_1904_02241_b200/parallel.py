@@ -495,6 +495,8 @@ class ShardedPageRank:
                     conv = True
                     break
         ex.end(e)
+        # a peer that missed its deadline invalidates every step since
+        _lib.check(eng.ctx._lib.gcb_peer_check(eng.ctx.handle), "peer exchange")
         if gather_ranks:
             ex.sync_full(ranks)
         return PrResult(ranks, it, conv)

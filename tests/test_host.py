@@ -220,10 +220,3 @@ class TestUtil:
 
     def test_checksum(self):
         assert gcb.result_checksum(np.zeros(3)) == orc.checksum(np.zeros(3))
-
-    def test_map_ordered(self):
-        from paper_1904_02241_b200.util import map_ordered
-        items = list(range(50))
-        for threads in (1, 4):
-            assert map_ordered(lambda x: x * x, items, threads) == [x * x for x in items]
-        assert map_ordered(str, [], 4) == []
