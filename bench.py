@@ -53,7 +53,10 @@ def parse_args():
     p.add_argument("--f32-values", action="store_true")
     p.add_argument("--exact", action="store_true")
     p.add_argument("--no-l2-window", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--cpu-seconds", type=float, default=12.0,
+                   help="bounded CPU sample of our arm's cpu_baseline (at least one call)")
+    p.add_argument("--ref-seconds", type=float, default=150.0,
+                   help="reference arm: stop timing further calls after this many seconds")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -130,22 +133,36 @@ class ClockSampler:
 # CPU leg (oracle port) -- test infrastructure, only a reported baseline
 # ---------------------------------------------------------------------------
 
-def cpu_pagerank_sample(arenas, n, m, budget_s, threads, direction="pull"):
-    """Run oracle pr_blocked iterations (1 per call, OpenMP over rows) until
-    ``budget_s`` has elapsed; returns (GTEPS, iterations, seconds)."""
+def cpu_pagerank_sample(arenas, n, m, budget_s, threads, iters, direction="pull"):
+    """The reference's run contract (cli.py:199-211, 256-262): whole
+    pr_blocked calls of ``iters`` iterations (tol 0), out-degrees counted once
+    per call (kernels.py:373-374), on the oracle C port with OpenMP, until
+    ``budget_s`` has elapsed (at least one call).  Returns (GTEPS, calls,
+    seconds, ranks of the last call, per-call setup seconds)."""
     from oracle import oracle as orc
 
     bg = orc.Blocked(direction, 0, n, m, *arenas)
-    done, spent = 0, 0.0
+    # per-call setup (degree count, allocations): a 1-iteration call minus one
+    # iteration of a full call
+    t0 = time.perf_counter()
+    orc.pr_blocked(bg, tol=0.0, max_iters=1, threads=threads)
+    t1 = time.perf_counter() - t0
+    done, spent, out = 0, 0.0, None
     while spent < budget_s or done == 0:
         t0 = time.perf_counter()
-        orc.pr_blocked(bg, tol=0.0, max_iters=1, threads=threads)
+        out = orc.pr_blocked(bg, tol=0.0, max_iters=iters, threads=threads)
         spent += time.perf_counter() - t0
         done += 1
-    return m * done / spent / 1e9, done, spent
+    per_call = spent / done
+    setup = max(0.0, t1 - (per_call - t1) / max(1, iters - 1)) if iters > 1 else 0.0
+    return m * iters * done / spent / 1e9, done, spent, out.ranks, setup
 
 
 def run_reference(args):
+    """The reference arm: the CPU implementation of the path (the oracle C
+    port of pr_blocked, bit-identical to the reference's numba path), timed on
+    the reference's own contract -- one step = one pr_blocked call of
+    ``--iters`` iterations (cli.py:256-262) -- with every host thread."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -159,35 +176,47 @@ def run_reference(args):
     setup_s = time.perf_counter() - t0
     n, m = src.n, src.m
     del src
-    arenas = (bg.row_starts, bg.lro_arena, bg.id_map_arena, bg.edge_starts, bg.col_arena)
-    for _ in range(args.warmup):
-        orc.pr_blocked(bg, tol=0.0, max_iters=1, threads=threads)
+    # per-call setup, reported apart from the per-iteration rate
+    t = time.perf_counter()
+    orc.pr_blocked(bg, tol=0.0, max_iters=1, threads=threads)
+    t1 = time.perf_counter() - t
+    # warm-up calls (page faults, OpenMP pool); bounded: CPU calls take seconds
+    for _ in range(min(args.warmup, 2)):
+        orc.pr_blocked(bg, tol=0.0, max_iters=args.iters, threads=threads)
     times = []
+    t_start = time.perf_counter()
     for _ in range(args.steps):
         t = time.perf_counter()
-        orc.pr_blocked(bg, tol=0.0, max_iters=1, threads=threads)
+        orc.pr_blocked(bg, tol=0.0, max_iters=args.iters, threads=threads)
         times.append(time.perf_counter() - t)
-    del arenas
+        if time.perf_counter() - t_start > args.ref_seconds:
+            break  # keep the arm within a few minutes; steps says how many ran
     t_step = float(np.mean(times))
-    value = m / t_step / 1e9
-    sample = (f"{args.steps} steps x 1 PageRank iteration of rmat:{args.scale}:"
-              f"{args.edge_factor}:{args.seed} pull TOCAB W={args.width} (full graph); "
-              f"oracle setup {setup_s:.1f}s untimed")
+    value = m * args.iters / t_step / 1e9
+    per_iter = (t_step - t1) / max(1, args.iters - 1) if args.iters > 1 else t_step
+    call_setup = max(0.0, t1 - per_iter)
+    sample = (f"{len(times)} pr_blocked calls x {args.iters} iterations (tol 0) of rmat:{args.scale}:"
+              f"{args.edge_factor}:{args.seed} {args.direction} TOCAB W={args.width} (full graph), "
+              f"oracle C port with OpenMP ({threads} threads); per-call setup "
+              f"{call_setup * 1e3:.0f} ms of {t_step * 1e3:.0f} ms; graph build {setup_s:.1f}s untimed")
     line = {
         "metric": "PageRank GTEPS per iteration", "value": round(value, 6), "unit": "GTEPS",
-        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "impl": "reference", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": len(times), "warmup": min(args.warmup, 2),
         "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic R-MAT (reference generator)",
-        "config": workload_config(args, n, m),
+        "config": workload_config(args, n, m, int(os.environ.get("WORLD_SIZE", "1"))),
         "cpu_baseline": {"value": round(value, 6), "unit": "GTEPS", "cores": threads,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample,
+                         "ms_per_iteration": round(per_iter * 1e3, 3),
+                         "ms_setup_per_call": round(call_setup * 1e3, 3)},
         "e2e": {"value": round(value, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, n, m):
+def workload_config(args, n, m, world):
     return {
         "workload": (f"pagerank-{args.direction}-tocab rmat:{args.scale}:{args.edge_factor}:"
                      f"{args.seed} {args.iters} iterations/step"),
@@ -195,13 +224,13 @@ def workload_config(args, n, m):
         "num_vertices": n, "num_edges": m, "width": args.width,
         "layout": ("steady state: degree-ordered copy with hybrid edge classes, built in the "
                    "untimed warm-up (e2e: hot-bit layout of each freshly uploaded graph)"
-                   if args.gpus == 1 and not args.exact and not args.f32_values else
+                   if world == 1 and not args.exact and not args.f32_values else
                    "as built by the call path (no promotion)"),
         "iterations_per_step": args.iters, "damping": 0.85, "tol": 0.0,
         "direction": args.direction, "value_dtype": "f32" if args.f32_values else "f64",
         "l2": "inputs larger than L2 (col arena 4|E| bytes >> 126 MB)",
-        "parallelism": (f"destination shards x{args.gpus} (cuts balance in-edges + 4 x vertices), "
-                        "contribution exchange per config.exchange" if args.gpus > 1 else "single GPU"),
+        "parallelism": (f"destination shards x{world} (cuts balance in-edges + 4 x vertices), "
+                        "contribution exchange per config.exchange" if world > 1 else "single GPU"),
     }
 
 
@@ -218,6 +247,9 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                         "(bench.py --gpus N without torchrun starts them itself)")
     # GCB_DEVICE / GCB_DIST_BACKEND let the multi-rank path be smoke-tested
     # with several ranks on one GPU (gloo); production is one rank per GPU, NCCL
     local = int(os.environ.get("GCB_DEVICE", os.environ.get("LOCAL_RANK", "0")))
@@ -344,16 +376,19 @@ def run_ours(args):
     prof = ctx.read_profile()
     ctx.set_profiling(False)
     per_iter = {k: v[0] / (prof_steps * args.iters) for k, v in prof.items()}
-    gather_ms = per_iter["gather"]
-    gather_groups = prof["gather"][1] / (prof_steps * args.iters)
+    pull_ms = per_iter["gather"]
+    hub_ms = per_iter["hub_push"]
+    gather_ms = pull_ms + hub_ms
+    gather_groups = (prof["gather"][1] + prof["hub_push"][1]) / (prof_steps * args.iters)
 
     peak, peak_kind = measured_hbm_peak()
     peak *= world  # aggregate HBM of the job
     b_alg = algorithmic_bytes_pr(n, m)
     achieved = b_alg / t_iter_s / 1e9
-    # dominant kernel (the pull gather, k_pull_hot): SURVEY 8(d) per-edge and
-    # per-vertex bytes it must move -- col_idx 4 B/edge, the contribution read
-    # 8 B/vertex, the row pointer 4 B/vertex -- over the launches of one iteration
+    # dominant kernel (the pull gather, k_pull_hot, with the hybrid hub push
+    # pass k_push_hot): SURVEY 8(d) per-edge and per-vertex bytes it must move
+    # -- col_idx 4 B/edge, the contribution read 8 B/vertex, the row pointer
+    # 4 B/vertex -- over the launches of one iteration
     b_gather = 4 * m + 8 * n + 4 * (n + 1)
     gather_s = gather_ms / 1e3
     g_achieved = b_gather / gather_s / 1e9 if gather_ms else None
@@ -389,6 +424,18 @@ def run_ours(args):
         },
         "kernels_ms_per_iter": {k: round(v, 4) for k, v in per_iter.items()},
     }
+    if world == 1 and args.direction == "pull" and not args.exact:
+        roofline["requests"] = request_model(ctx, bg, pull_ms, hub_ms, clk)
+
+    # ---- parity of the timed output (cli.py:226-239 verifies every run) ----
+    parity = None
+    if world == 1 and not args.f32_values:
+        parity = timed_parity(ctx, bg, ranks, args, flags)
+
+    # ---- the layout a default API call runs (no promotion yet) ----
+    layouts = None
+    if world == 1 and not args.exact and not args.f32_values:
+        layouts = default_layout_rate(ctx, bg, stream, args, flags, value, ms_step)
 
     # ---- e2e: public host-buffer API, arenas from pinned memory each step ----
     e2e = None
@@ -401,14 +448,26 @@ def run_ours(args):
 
         arenas = (bg.row_starts, bg.lro_arena, bg.id_map_arena, bg.edge_starts, bg.col_arena)
         threads = orc.default_threads()
-        c_val, c_iters, c_s = cpu_pagerank_sample(arenas, n, m, args.cpu_seconds, threads,
-                                                  args.direction)
+        c_val, c_calls, c_s, c_ranks, c_setup = cpu_pagerank_sample(
+            arenas, n, m, args.cpu_seconds, threads, args.iters, args.direction)
         cpu = {"value": round(c_val, 6), "unit": "GTEPS", "cores": threads, "kind": "port",
-               "sample": f"{c_iters} PageRank iteration(s) of the same rmat:{args.scale} "
-                         f"TOCAB W={args.width} graph, oracle/ C port with OpenMP, "
-                         f"{c_s:.1f}s"}
+               "sample": f"{c_calls} pr_blocked call(s) x {args.iters} iterations of the same "
+                         f"rmat:{args.scale} TOCAB W={args.width} graph, oracle/ C port with "
+                         f"OpenMP, {c_s:.1f}s; per-call setup {c_setup * 1e3:.0f} ms"}
+        if parity is not None:
+            # the oracle restates the reference's pr_blocked bit for bit
+            # (tests/test_oracle.py): check the timed ranks against it too
+            h = ranks.cpu().numpy()
+            ex = parity.pop("_exact")
+            rel = np.abs(h - c_ranks) / np.abs(c_ranks)
+            parity["vs_oracle_max_rel"] = float(rel.max())
+            parity["vs_oracle_max_abs"] = float(np.abs(h - c_ranks).max())
+            parity["exact_bitwise_vs_oracle"] = bool(np.array_equal(ex, c_ranks))
+            parity["verify_cli"] = bool(parity["vs_oracle_max_abs"] <= 1e-10 * n)
+    if parity is not None:
+        parity.pop("_exact", None)
 
-    cfg = workload_config(args, n, m)
+    cfg = workload_config(args, n, m, world)
     if world > 1:
         cfg["width"] = int(bg.width)  # rank 0's shard width (auto: DeviceShard._auto_width)
         if getattr(exchange, "fused", False):
@@ -426,6 +485,7 @@ def run_ours(args):
             "data": "synthetic R-MAT generated on device (bit-exact with the reference)",
             "config": cfg,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "parity": parity, "layouts": layouts,
             "gpu_launches": launches, "clocks": clk,
             "setup_s": round(setup_s, 2),
         }
@@ -433,6 +493,94 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# Random 8-byte LDG rate of one SM from an L2-resident vector, measured by
+# scripts/mb_gather.cu on this B200 (DESIGN 4.1): the request ceiling of the
+# L1TEX -> XBAR path that bounds every cold gather.
+GATHERS_PER_SM_CYCLE = 0.93
+
+
+def request_model(ctx, bg, pull_ms, hub_ms, clk):
+    """Cold gathers per iteration against the request ceiling: the pull pass
+    issues one L2 request per cold edge, so its floor is cold /
+    (0.93 x SMs x clock); request_frac = that floor / the measured pull time."""
+    out = (ctypes.c_int64 * 4)()
+    from paper_1904_02241_b200 import _lib
+
+    _lib.check(ctx._lib.gcb_blocked_gather_census(ctx.handle, bg.device().raw, out), "census")
+    hot, cold, hub, relabeled = (int(x) for x in out)
+    sms = ctx.info()["num_sms"] if hasattr(ctx, "info") else 148
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    floor_ms = cold / (GATHERS_PER_SM_CYCLE * sms * mhz * 1e6) * 1e3
+    total = hot + cold + hub
+    return {"hot_table_edges": hot, "cold_edges": cold, "hub_push_edges": hub,
+            "cold_share": round(cold / total, 4) if total else None,
+            "layout": "degree-ordered + hybrid" if relabeled else "hot-bit",
+            "pull_ms_per_iteration": round(pull_ms, 4),
+            "hub_push_ms_per_iteration": round(hub_ms, 4),
+            "request_floor_ms": round(floor_ms, 4),
+            "request_frac": round(floor_ms / pull_ms, 4) if pull_ms else None,
+            "model": f"cold edges / ({GATHERS_PER_SM_CYCLE} gathers per SM-cycle x {sms} SMs x "
+                     f"{mhz:.0f} MHz); 0.93 = scripts/mb_gather.cu random-LDG ceiling"}
+
+
+def timed_parity(ctx, bg, ranks, args, flags):
+    """The timed steps' ranks against one exact-mode call on the same graph
+    (bit-identical to the reference: tests/test_gpu_parity.py, and checked
+    against the oracle below when the CPU leg runs)."""
+    import torch
+
+    from paper_1904_02241_b200 import _lib
+
+    ex = torch.empty_like(ranks)
+    it, cv = ctypes.c_int(), ctypes.c_int()
+    _lib.check(ctx._lib.gcb_pr_blocked_dev(ctx.handle, bg.device().raw, 0.85, 0.0, args.iters,
+                                           flags | _lib.FLAG_EXACT, ctypes.c_void_p(ex.data_ptr()),
+                                           ctypes.byref(it), ctypes.byref(cv)))
+    torch.cuda.synchronize()
+    rel = ((ranks - ex).abs() / ex.abs()).max().item()
+    return {"vs_exact_max_rel": rel, "tolerance": 1e-6, "pass": bool(rel <= 1e-6),
+            "reference": "exact mode (reference operation order) on the same device graph",
+            "_exact": ex.cpu().numpy()}
+
+
+def default_layout_rate(ctx, bg, stream, args, flags, value, ms_step):
+    """Steady state of the layout a default API call runs before promotion
+    (GCB_RELABEL_AFTER = 4096 fast iterations): the hot-bit layout of the
+    graph as partitioned.  Same step, timed the same way."""
+    import torch
+
+    from paper_1904_02241_b200 import _lib
+
+    n, m = bg.num_vertices, bg.num_edges
+    out = torch.empty(n, dtype=torch.float64, device=stream.device)
+    it, cv = ctypes.c_int(), ctypes.c_int()
+    f = flags | _lib.FLAG_NO_RELABEL
+
+    def step():
+        _lib.check(ctx._lib.gcb_pr_blocked_dev(ctx.handle, bg.device().raw, 0.85, 0.0, args.iters,
+                                               f, ctypes.c_void_p(out.data_ptr()),
+                                               ctypes.byref(it), ctypes.byref(cv)))
+
+    for _ in range(3):
+        step()
+    k = max(3, min(10, args.steps))
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    return {"timed": {"layout": "degree-ordered copy + hybrid hub push (promoted)",
+                      "value": round(value, 3), "ms_per_step": round(ms_step, 4)},
+            "default_api": {"layout": "hot-bit layout of the graph as partitioned (before "
+                                      "promotion at 4096 fast iterations)",
+                            "value": round(m * args.iters / (ms / 1e3) / 1e9, 3),
+                            "ms_per_step": round(ms, 4), "steps": k}}
 
 
 def run_e2e(args, bg, ctx, stream, flags, steps=None):
@@ -498,8 +646,24 @@ def auto_width(args) -> int:
     return w
 
 
+def launch_ranks(args) -> int:
+    """--gpus N outside torchrun: start one rank per GPU the way the driver
+    does (torch.distributed.run, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
     if args.width <= 0:
         args.width = auto_width(args)
     if args.impl == "reference":

@@ -15,7 +15,8 @@
  *  - Every function returns GCB_OK (0) or an error code; gcb_last_error()
  *    returns a thread-local message for the last failure.
  *      GCB_EINVAL (1) -> ValueError, GCB_ECUDA (2) -> RuntimeError,
- *      GCB_ENOMEM (3) -> MemoryError, GCB_EINDEX (4) -> IndexError.
+ *      GCB_ENOMEM (3) -> MemoryError, GCB_EINDEX (4) -> IndexError,
+ *      GCB_EFORMAT (5) -> GraphFormatError (a ValueError), GCB_EIO (6) -> OSError.
  *  - Plain pointers and sizes only.  Pointers named *_host are host memory,
  *    borrowed for the duration of the call; pointers named *_dev are device
  *    memory on the context's device.  Host-buffer calls are synchronous on
@@ -43,6 +44,8 @@ extern "C" {
 #define GCB_ECUDA 2
 #define GCB_ENOMEM 3
 #define GCB_EINDEX 4
+#define GCB_EFORMAT 5
+#define GCB_EIO 6
 
 #define GCB_DIR_PULL 0
 #define GCB_DIR_PUSH 1
@@ -129,6 +132,12 @@ int gcb_partition_cb(gcb_ctx *ctx, const gcb_csr *g, int64_t width, gcb_blocked 
 /* mask_dev[n] (device bytes) = 1 for every source the blocking's edges read:
  * the per-rank need set of the sparse contribution exchange. */
 int gcb_blocked_source_mask(gcb_ctx *ctx, const gcb_blocked *bg, uint8_t *mask_dev);
+/* Request model of the fast pull gather (no reference counterpart; feeds
+ * bench.py's roofline.request_frac): out4 = {edges served from the
+ * shared-memory hot table, cold edges (one L2 request each), hub-destination
+ * edges of the hybrid push pass, 1 if the degree-ordered copy is the layout}.
+ * Counts the layout the fast pull runs (the promoted copy when one exists). */
+int gcb_blocked_gather_census(gcb_ctx *ctx, gcb_blocked *bg, int64_t *out4);
 /* Marks an uploaded pull blocking as cb-scheme (arenas already in that layout). */
 int gcb_blocked_mark_cb(gcb_ctx *ctx, gcb_blocked *bg);
 /* BlockedGraph(...) blocking.py:86-110 from host arenas (int64 lro converted
@@ -149,6 +158,16 @@ int gcb_blocked_download(gcb_ctx *ctx, const gcb_blocked *bg, int64_t *row_start
 int gcb_blocked_range_bounds(gcb_ctx *ctx, gcb_blocked *bg, int64_t k,
                              int64_t *bounds_host);
 int gcb_blocked_destroy(gcb_blocked *bg);
+/* GCB container (blocking.py:327-441), written from and read into device
+ * arenas (csrc/gcbio.cu): write_gcb blocking.py:341-365 and read_gcb
+ * blocking.py:368-441, byte-identical files and the same checks in the same
+ * order (truncated, CRC, magic, direction, block table, trailing bytes, edge
+ * totals; GCB_EFORMAT).  The CRC-32 (zlib's) is computed on the device. */
+int gcb_blocked_save(gcb_ctx *ctx, gcb_blocked *bg, const char *path);
+int gcb_blocked_load(gcb_ctx *ctx, const char *path, gcb_blocked **out);
+int gcb_blocked_scheme(const gcb_blocked *bg, int *is_cb);
+/* zlib.crc32 of a host buffer, computed on the device (the container's check) */
+int gcb_crc32(gcb_ctx *ctx, const void *data_host, int64_t len, uint32_t *crc);
 
 /* ---- value kernels (kernels.py) ----------------------------------------- */
 /* compute_contributions kernels.py:185-191: out = deg > 0 ? rank / deg : 0 */

@@ -16,7 +16,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgcb_b200.so")
 
-GCB_OK, GCB_EINVAL, GCB_ECUDA, GCB_ENOMEM, GCB_EINDEX = 0, 1, 2, 3, 4
+GCB_OK, GCB_EINVAL, GCB_ECUDA, GCB_ENOMEM, GCB_EINDEX, GCB_EFORMAT, GCB_EIO = 0, 1, 2, 3, 4, 5, 6
 DIR_PULL, DIR_PUSH = 0, 1
 FLAG_EXACT = 1
 FLAG_F32_VALUES = 2
@@ -78,6 +78,11 @@ SIGNATURES = {
     "gcb_partition_cb": ([c_vp, c_vp, c_i64, PP], c_int),
     "gcb_blocked_mark_cb": ([c_vp, c_vp], c_int),
     "gcb_blocked_source_mask": ([c_vp, c_vp, c_vp], c_int),
+    "gcb_blocked_gather_census": ([c_vp, c_vp, P_i64], c_int),
+    "gcb_blocked_save": ([c_vp, c_vp, ctypes.c_char_p], c_int),
+    "gcb_blocked_load": ([c_vp, ctypes.c_char_p, PP], c_int),
+    "gcb_blocked_scheme": ([c_vp, P_int], c_int),
+    "gcb_crc32": ([c_vp, c_vp, c_i64, P_u32], c_int),
     "gcb_blocked_upload": ([c_vp, c_int, c_i64, c_i64, c_i64, c_i64, P_i64, P_i64, P_u32, P_i64,
                             P_u32, P_dbl, PP], c_int),
     "gcb_blocked_info": ([c_vp, P_int, P_i64, P_i64, P_i64, P_i64, P_i64, P_int], c_int),
@@ -149,6 +154,15 @@ def check(rc: int, what: str = ""):
         raise IndexError(msg)
     if rc == GCB_ENOMEM:
         raise MemoryError(text)
+    if rc == GCB_EFORMAT:
+        from .graph import GraphFormatError
+
+        raise GraphFormatError(msg)
+    if rc == GCB_EIO:
+        import re
+
+        e = re.search(r"\[errno (\d+)\]", msg)
+        raise OSError(int(e.group(1)) if e else 0, msg)  # errno picks the subclass
     raise GcbError(text)
 
 
@@ -212,7 +226,8 @@ class Context:
         ms = (ctypes.c_double * 4)()
         cnt = (ctypes.c_int64 * 4)()
         check(self._lib.gcb_ctx_read_profile(self.handle, ms, cnt))
-        names = ("gather", "fixup", "merge", "other")
+        # gcb_internal.cuh ProfScope categories
+        names = ("gather", "hub_push", "update", "other")
         return {k: (ms[i], cnt[i]) for i, k in enumerate(names)}
 
     def bind_torch_stream(self):

@@ -13,8 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import dataclasses
-import struct
-import zlib
+import os
 
 import numpy as np
 
@@ -35,11 +34,8 @@ __all__ = [
     "read_gcb",
 ]
 
-GCB_MAGIC = b"GCB1"
 DEFAULT_BLOCK_WIDTH = 1 << 18  # blocking.py:49
 DEGREE_BINS = ((0, 7), (8, 15), (16, 31), (32, None))
-_FLAG_WEIGHTS = 1
-_FLAG_CB = 2
 
 
 @dataclasses.dataclass(eq=False, repr=False)
@@ -322,77 +318,26 @@ def block_stats(bg: BlockedGraph) -> BlockStats:
 
 
 # ---------------------------------------------------------------------------
-# GCB container (blocking.py:327-441): same little-endian layout + CRC32
+# GCB container (blocking.py:327-441): the reference's file format, written
+# from and read into device arenas by csrc/gcbio.cu (CRC-32 on the device)
 # ---------------------------------------------------------------------------
 
-_HEADER = struct.Struct("<4sBBH4Q")
-
-
 def write_gcb(bg: BlockedGraph, path) -> None:
-    flags = (_FLAG_WEIGHTS if bg.weighted else 0) | (_FLAG_CB if bg.scheme == "cb" else 0)
-    chunks = [_HEADER.pack(GCB_MAGIC, 0 if bg.direction == "pull" else 1, flags, 0,
-                           bg.num_vertices, bg.num_edges, bg.width, bg.num_blocks)]
-    for blk in bg.blocks():
-        chunks.append(struct.pack("<2Q", blk.n_local, blk.num_edges))
-        chunks.append(np.asarray(blk.id_map, dtype="<u4").tobytes())
-        chunks.append(np.asarray(blk.local_row_offsets, dtype="<u8").tobytes())
-        chunks.append(np.asarray(blk.col_indices, dtype="<u4").tobytes())
-        if bg.weighted:
-            chunks.append(np.asarray(blk.edge_weights, dtype="<f8").tobytes())
-    body = b"".join(chunks)
-    with open(path, "wb") as fh:
-        fh.write(body)
-        fh.write(struct.pack("<I", zlib.crc32(body) & 0xFFFFFFFF))
+    """write_gcb blocking.py:341-365: byte-identical container."""
+    h = bg.device()
+    _lib.check(h.ctx._lib.gcb_blocked_save(h.ctx.handle, h.raw, os.fsencode(path)), "write_gcb")
 
 
 def read_gcb(path) -> BlockedGraph:
-    with open(path, "rb") as fh:
-        blob = fh.read()
-    if len(blob) < _HEADER.size + 4:
-        raise GraphFormatError(f"{path}: truncated container")
-    body = blob[:-4]
-    (crc,) = struct.unpack("<I", blob[-4:])
-    if zlib.crc32(body) & 0xFFFFFFFF != crc:
-        raise GraphFormatError(f"{path}: CRC mismatch, file is corrupt")
-    magic, dcode, flags, _, n, m, width, B = _HEADER.unpack_from(body, 0)
-    if magic != GCB_MAGIC:
-        raise GraphFormatError(f"{path}: bad magic {magic!r}")
-    if dcode not in (0, 1):
-        raise GraphFormatError(f"{path}: bad direction byte {dcode}")
-    weighted = bool(flags & _FLAG_WEIGHTS)
-    at = _HEADER.size
-    ids, lros, cols, wts = [], [], [], []
-    rows = np.zeros(B, dtype=np.int64)
-    edges = np.zeros(B, dtype=np.int64)
-
-    def take(dtype, count):
-        nonlocal at
-        arr = np.frombuffer(body, dtype=dtype, count=count, offset=at)
-        at += arr.nbytes
-        return arr
-
-    for b in range(B):
-        if at + 16 > len(body):
-            raise GraphFormatError(f"{path}: truncated block table")
-        nl, ne = struct.unpack_from("<2Q", body, at)
-        at += 16
-        rows[b], edges[b] = nl, ne
-        ids.append(take("<u4", nl))
-        lro = take("<u8", nl + 1)
-        if ne != int(lro[-1]):
-            raise GraphFormatError(f"{path}: block {b} edge count disagrees")
-        lros.append(lro.astype(np.int64))
-        cols.append(take("<u4", ne))
-        if weighted:
-            wts.append(take("<f8", ne))
-    if at != len(body):
-        raise GraphFormatError(f"{path}: trailing bytes after last block")
-    rs = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
-    es = np.concatenate([[0], np.cumsum(edges)]).astype(np.int64)
-    if int(es[-1]) != m:
-        raise GraphFormatError(f"{path}: total edges disagree with header")
-    cat = lambda parts, dt: (np.concatenate(parts).astype(dt) if parts else np.zeros(0, dt))
-    return BlockedGraph("pull" if dcode == 0 else "push", "cb" if flags & _FLAG_CB else "tocab",
-                        int(width), int(n), int(m), rs, cat(lros, np.int64),
-                        cat(ids, np.uint32), es, cat(cols, np.uint32),
-                        np.concatenate(wts) if weighted and wts else None)
+    """read_gcb blocking.py:368-441: GraphFormatError on a truncated or
+    corrupt container, checked in the reference's order."""
+    ctx = _lib.context()
+    raw = ctypes.c_void_p()
+    _lib.check(ctx._lib.gcb_blocked_load(ctx.handle, os.fsencode(path), ctypes.byref(raw)))
+    is_cb = ctypes.c_int()
+    try:
+        _lib.check(ctx._lib.gcb_blocked_scheme(raw, ctypes.byref(is_cb)))
+    except Exception:
+        ctx._lib.gcb_blocked_destroy(raw)
+        raise
+    return BlockedGraph._from_device(ctx, raw, scheme="cb" if is_cb.value else "tocab")

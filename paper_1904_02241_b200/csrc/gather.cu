@@ -385,4 +385,56 @@ void gather_accum(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, bool use_we
   }
 }
 
+// Census of one block's arena for the request model: edges whose source is
+// served from the shared-memory hot table (HOTBIT: recoded entries; else the
+// block's degree-ordered prefix [lo, lo + hot)).
+__global__ void k_count_hot(int64_t es, int64_t ee, const uint32_t *__restrict__ col, bool hotbit,
+                            uint32_t lo, uint32_t hot, unsigned long long *__restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t e = es + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ee;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = col[e];
+    c += hotbit ? (x >> 31) : ((x - lo) < hot ? 1u : 0u);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 }  // namespace gcb
+
+using namespace gcb;
+
+extern "C" {
+
+int gcb_blocked_gather_census(gcb_ctx *ctx, gcb_blocked *bg, int64_t *out4) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bg && out4, "NULL argument");
+  GCB_REQUIRE(bg->direction == 0 && !bg->cb, "the census is of a pull TOCAB blocking");
+  DeviceGuard dg(ctx->device);
+  // the layout the fast pull runs: the degree-ordered copy once promoted
+  gcb_blocked *x = bg->rl ? bg->rl : bg;
+  ensure_exec(ctx, x);
+  const bool hotbit = !x->is_relabeled && x->hot_k > 0;
+  DArray<unsigned long long> cnt(1);
+  GCB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
+  for (int64_t b = 0; b < x->B && x->hot_k > 0; ++b) {
+    const int64_t es = x->h_edge_starts[b], ee = x->h_edge_starts[b + 1];
+    if (ee == es) continue;
+    const int64_t lo = b * x->width, hi = (lo + x->width < x->n) ? lo + x->width : x->n;
+    const int64_t hot = x->hot_k < hi - lo ? x->hot_k : hi - lo;
+    k_count_hot<<<grid_for(ee - es, 256, 65536), 256, 0, ctx->stream>>>(
+        es, ee, hotbit ? x->xcol.p : x->col.p, hotbit, (uint32_t)lo, (uint32_t)hot, cnt.p);
+    after_launch(ctx, "k_count_hot");
+  }
+  unsigned long long h = 0;
+  d2h(ctx, &h, cnt.p, 1);
+  sync(ctx);
+  out4[0] = (int64_t)h;                          // hot-table edges (shared memory)
+  out4[1] = x->m - (int64_t)h;                   // cold edges: one L2 request each
+  out4[2] = x->hybrid ? x->hybrid->m : 0;        // hub-destination edges (push pass)
+  out4[3] = x->is_relabeled ? 1 : 0;             // layout: 1 degree-ordered, 0 hot-bit
+  GCB_API_END
+}
+
+}  // extern "C"

@@ -259,7 +259,8 @@ inline void after_launch(gcb_ctx *ctx, const char *name) {
 }
 
 // Records CUDA events around a group of launches when profiling is on.
-// Categories: 0 gather/scatter, 1 carry fix-up, 2 merge/update, 3 other.
+// Categories: 0 gather/scatter, 1 hybrid hub-destination push pass,
+// 2 merge/update, 3 other.
 struct ProfScope {
   gcb_ctx *ctx;
   int cat;

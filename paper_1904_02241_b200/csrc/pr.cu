@@ -1124,7 +1124,7 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
     } else if (!push) {
       pull_sums(ctx, bg, contrib, contrib32, false, flags, -1, bg->sums.p, true);
       if (bg->hybrid) {  // relabel.cu: cold-source -> hot-destination edges
-        ProfScope ps(ctx, 0);
+        ProfScope ps(ctx, 1);
         push_scatter(ctx, bg->hybrid, contrib, bg->sums.p, false, flags, -1, true);
       }
     } else {

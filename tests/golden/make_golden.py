@@ -4,15 +4,19 @@ Usage (needs /root/reference, which does not exist on the GPU box):
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba \
         python tests/golden/make_golden.py
 
-Writes tests/golden/small.npz (arrays from a few small graphs) and
+Writes tests/golden/small.npz (arrays from a few small graphs),
 tests/golden/checksums.json (sha256[:16] via gcb.util.result_checksum for the
-rmat:16:16:1 configuration that BASELINE.md / SURVEY.md 8c quote).
+rmat:16:16:1 configuration that BASELINE.md / SURVEY.md 8c quote) and
+tests/golden/gcb/*.gcb (containers written by the reference's write_gcb,
+blocking.py:341-365: pull, push, weighted and cb blockings of rmat:10:8:1).
+``--gcb-only`` rewrites just the containers.
 """
 import json
 import os
+import sys
 
 import numpy as np
-from gcb.blocking import partition_cb, partition_tocab
+from gcb.blocking import partition_cb, partition_tocab, write_gcb
 from gcb.graph import GraphGenSpec, from_edges, generate, symmetrize, transpose
 from gcb.kernels import PrParams, pr_baseline, pr_blocked, spmv, spmv_blocked
 from gcb.traversal import DirectionPolicy, bc, bc_backward, bc_single_source, bfs, sample_sources
@@ -35,7 +39,34 @@ def blocked_arrays(prefix, bg, store):
         store[prefix + "weight_arena"] = bg.weight_arena
 
 
+def gcb_files():
+    """Reference-written GCB containers: the byte-identity fixtures of
+    write_gcb / read_gcb (tests/test_gpu_parity.py TestGcbContainer)."""
+    d = os.path.join(OUT, "gcb")
+    os.makedirs(d, exist_ok=True)
+    g = gen("rmat:10:8:1")
+    gt = transpose(g)
+    w = np.random.default_rng(0).random(g.num_edges)
+    gw = from_edges(g.edge_sources(), g.col_indices, num_vertices=g.num_vertices, weights=w)
+    cases = {
+        "r10_pull64": partition_tocab(gt, "pull", 64),
+        "r10_push1000": partition_tocab(g, "push", 1000),
+        "r10w_pull64": partition_tocab(transpose(gw), "pull", 64),
+        "r10w_push64": partition_tocab(gw, "push", 64),
+        "r10_cb64": partition_cb(gt, 64),
+        "r10w_cb1000": partition_cb(transpose(gw), 1000),
+        "empty_pull8": partition_tocab(from_edges([], [], num_vertices=5), "pull", 8),
+    }
+    for name, bg in cases.items():
+        write_gcb(bg, os.path.join(d, name + ".gcb"))
+    print("wrote", sorted(cases))
+
+
 def main():
+    if "--gcb-only" in sys.argv:
+        gcb_files()
+        return
+    gcb_files()
     s = {}
     # --- rmat:10:8:1 (n=1024, m=8192) --------------------------------------
     g = gen("rmat:10:8:1")

@@ -10,9 +10,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def run_bench(*args, env=None):
+    full = {**os.environ, **(env or {})}
+    full = {k: v for k, v in full.items() if v is not None}
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT,
-                         capture_output=True, text=True, timeout=300,
-                         env={**os.environ, **(env or {})})
+                         capture_output=True, text=True, timeout=300, env=full)
     assert out.returncode == 0, out.stderr[-2000:]
     return out.stdout.strip().splitlines()
 
@@ -39,3 +40,34 @@ def test_reference_arm_silent_on_other_ranks():
     # under torchrun only rank 0 runs and prints; the others exit 0 without work
     assert run_bench("--impl", "reference", "--scale", "10", "--steps", "1", "--warmup", "1",
                      env={"RANK": "1", "WORLD_SIZE": "2"}) == []
+
+
+def test_reference_arm_times_whole_calls():
+    # one step = one pr_blocked call of --iters iterations (cli.py:256-262),
+    # the same work the GPU arm times; per-call setup is reported apart
+    d = json.loads(run_bench("--impl", "reference", "--scale", "12", "--steps", "2", "--warmup",
+                             "1", "--iters", "10")[0])
+    cb = d["cpu_baseline"]
+    assert "x 10 iterations" in cb["sample"]
+    assert d["config"]["iterations_per_step"] == 10
+    assert cb["ms_per_iteration"] > 0 and cb["ms_setup_per_call"] >= 0
+    # value = |E| x iterations / step time
+    assert abs(d["value"] - 16 * 4096 * 10 / (d["ms_per_step"] / 1e3) / 1e9) <= 1e-3 * d["value"] + 1e-6
+
+
+def test_gpus_flag_must_match_world():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--steps", "1", "--warmup", "1", "--scale", "10"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=300,
+                         env={**os.environ, "WORLD_SIZE": "1", "RANK": "0"})
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
+
+
+def test_gpus_flag_launches_ranks():
+    # --gpus 2 outside torchrun starts two ranks itself; the reference arm
+    # prints one line from rank 0 and reports the job's world size
+    lines = run_bench("--impl", "reference", "--gpus", "2", "--scale", "10", "--steps", "1",
+                      "--warmup", "1", env={"WORLD_SIZE": None, "RANK": None})
+    lines = [x for x in lines if x.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2

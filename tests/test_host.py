@@ -176,33 +176,6 @@ class TestBlockingHost:
             bg.block(bg.num_blocks)
         assert bg.value_range(bg.num_blocks - 1)[1] == g.n
 
-    @pytest.mark.parametrize("direction,weights", [("pull", False), ("push", False),
-                                                   ("pull", True)])
-    def test_gcb_roundtrip(self, tmp_path, direction, weights):
-        _, bg = oracle_blocked(direction=direction, weights=weights)
-        p = tmp_path / "g.gcb"
-        gcb.write_gcb(bg, p)
-        back = gcb.read_gcb(p)
-        for name in ("row_starts", "lro_arena", "id_map_arena", "edge_starts", "col_arena"):
-            assert np.array_equal(getattr(back, name), getattr(bg, name))
-        assert back.direction == direction and back.weighted == weights
-        blob = bytearray(p.read_bytes())
-        blob[len(blob) // 2] ^= 0xFF
-        p.write_bytes(bytes(blob))
-        with pytest.raises(gcb.GraphFormatError):
-            gcb.read_gcb(p)
-
-    def test_gcb_matches_reference_bytes(self, tmp_path, golden):
-        """A file written by us parses back to the reference's arenas."""
-        bg = gcb.BlockedGraph("pull", "tocab", 64, 1024, 8192,
-                              golden["r10_pull64_row_starts"], golden["r10_pull64_lro_arena"],
-                              golden["r10_pull64_id_map_arena"], golden["r10_pull64_edge_starts"],
-                              golden["r10_pull64_col_arena"])
-        p = tmp_path / "r.gcb"
-        gcb.write_gcb(bg, p)
-        back = gcb.read_gcb(p)
-        assert np.array_equal(back.lro_arena, golden["r10_pull64_lro_arena"])
-
     def test_partition_arg_errors(self):
         g = gcb.CsrGraph(3, 2, [0, 1, 2, 2], [1, 2])
         with pytest.raises(ValueError):

@@ -2,6 +2,8 @@
 importing the reference (tests/golden/make_golden.py) and the sha256
 checksums SURVEY.md section 8c records.  CPU only."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -239,3 +241,15 @@ def test_partition_cb_golden(golden, r10, W):
         assert np.array_equal(getattr(bg, name), golden[f"r10_cb{W}_{name}"]), name
     # _cb_sums adds +0.0 for empty rows: ranks equal the TOCAB pull ones bitwise
     assert np.array_equal(golden[f"r10_cb{W}_pr10"], golden[f"r10_pull{W}_pr10"])
+
+
+def test_gcb_fixtures_pin_the_container_bytes():
+    """The reference-written containers (tests/golden/gcb/) equal the bytes the
+    oracle's restatement of write_gcb produces for the same blockings."""
+    from conftest import GCB_DIR, gcb_fixture_cases
+
+    cases = gcb_fixture_cases(orc)
+    assert sorted(os.listdir(GCB_DIR)) == sorted(k + ".gcb" for k in cases)
+    for name, (build, scheme) in cases.items():
+        with open(os.path.join(GCB_DIR, name + ".gcb"), "rb") as fh:
+            assert orc.gcb_bytes(build(), scheme) == fh.read(), name
