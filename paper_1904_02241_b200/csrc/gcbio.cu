@@ -9,7 +9,7 @@
 // weighted; trailing u32 zlib CRC-32 of every preceding byte.
 //
 // Save: the body is packed on the device (every section starts at a 4-byte
-// aligned offset: header 32 B, block header 16 B, sections 4/8 B per entry),
+// aligned offset: header 40 B, block header 16 B, sections 4/8 B per entry),
 // its CRC-32 computed on the device, then streamed to the file through two
 // pinned buffers (the D2H of chunk k+1 overlaps the write of chunk k).
 // Load: the file is streamed into a device body buffer the same way, the
@@ -39,7 +39,7 @@ constexpr int kLaneBytes = 256;                 // bytes per lane
 constexpr int64_t kChunk = 32 * kLaneBytes;     // 8 KiB per warp
 constexpr int kCrcWarps = 4;                    // warps per CTA
 constexpr int kMagicLen = 4;
-constexpr int64_t kHeaderBytes = 32;
+constexpr int64_t kHeaderBytes = 40;  // "<4sBBH4Q"
 constexpr uint8_t kFlagWeights = 1, kFlagCb = 2;
 
 struct CrcTables {

@@ -122,8 +122,8 @@ def test_corruption_detected(tmp_path, case, message):
         blob = reseal(body[:8] + struct.pack("<4Q", n, m, w, B + 1) + body[40:])
     elif case == "edges":
         # first block: n_edges one larger than its last local offset
-        nl, ne = struct.unpack_from("<QQ", body, 32)
-        blob = reseal(body[:32] + struct.pack("<QQ", nl, ne + 1) + body[48:])
+        nl, ne = struct.unpack_from("<QQ", body, 40)
+        blob = reseal(body[:40] + struct.pack("<QQ", nl, ne + 1) + body[56:])
     elif case == "trailing":
         blob = reseal(body + b"\0" * 8)
     else:
