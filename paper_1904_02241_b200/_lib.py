@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgcb_b200.so")
+# GCB_LIB: load another build of the library (scripts' ablation builds only)
+LIB_PATH = os.environ.get("GCB_LIB") or os.path.join(_HERE, "libgcb_b200.so")
 
 GCB_OK, GCB_EINVAL, GCB_ECUDA, GCB_ENOMEM, GCB_EINDEX, GCB_EFORMAT, GCB_EIO = 0, 1, 2, 3, 4, 5, 6
 DIR_PULL, DIR_PUSH = 0, 1

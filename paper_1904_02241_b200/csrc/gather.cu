@@ -50,11 +50,22 @@ constexpr uint32_t kHotBit = 0x80000000u;
 // compiler's if/else cost a BSSY/BSYNC pair per edge.
 //   HOTBIT: c is an xcol entry, hot iff bit 31 is set (slot = low bits);
 //   else  : c is a source id, hot iff c - lo < hot (degree-ordered prefix).
+#ifdef GCB_ABLATE
+// timing ablations (instrumented build only): bit 0 drop the row stores,
+// bit 1 drop the cold gathers, bit 2 one warp sum per tile instead of the
+// per-row reduction
+__constant__ int c_abl;
+#define ABL(b) ((c_abl >> (b)) & 1)
+#else
+#define ABL(b) 0
+#endif
+
 template <bool HOTBIT>
 __device__ __forceinline__ double gather_one(const double *vals, uint32_t c, uint32_t lo,
                                              uint32_t hot, uint32_t s_hot, uint64_t pol) {
   const uint32_t h = HOTBIT ? (c ^ kHotBit) : c - lo;
   double x;
+  if (ABL(1) && h >= hot) return 0.0;
   asm("{\n\t.reg .pred p;\n\t"
       "setp.lt.u32 p, %1, %2;\n\t"
       "@p ld.shared.f64 %0, [%3];\n\t"
@@ -130,10 +141,22 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (has_next && r0n + lane < Lb) idn = id_map_b[r0n + lane];
     s_ids[lane] = idl;
     __syncwarp();
+    if (ABL(2)) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc += v[k];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(FULL, acc, d);
+      if (lane == 0 && !ABL(0)) atomicAdd(out + s_ids[0], acc);
+    } else
     tile_reduce<double>(
         v, tbits, r0, lane, 0.0, [](double x, double y) { return __dadd_rn(x, y); },
         [&](uint32_t row, double x, uint32_t r_last) {
           const uint32_t rr = row - r0;
+          if (ABL(0)) {
+            if (x == 123.456) out[0] = x;  // keeps the reduction alive
+            return;
+          }
           const uint32_t vid = rr < 32 ? s_ids[rr] : id_map_b[row];
           if ((row == r0 && !tbits.first_start) || (row == r_last && tbits.last_cont))
             atomicAdd(out + vid, x);
@@ -340,6 +363,14 @@ static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double 
   const int pct = (int)(100.0 * carveout_kb() / 228.0 + 0.99);
   ensure_smem_attrs(ctx, (const void *)k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps>, smem,
                     pct > 100 ? 100 : pct);
+#ifdef GCB_ABLATE
+  {
+    const char *e = getenv("GCB_ABL");
+    const int abl = e ? atoi(e) : 0;
+    GCB_CUDA(cudaMemcpyToSymbolAsync(c_abl, &abl, sizeof(int), 0, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+  }
+#endif
   int64_t grid = ceil_div(nt, kGWarps);
   if (grid > ctx->num_sms) grid = ctx->num_sms;
   const double *hot_src = HOTBIT ? bg->hotval.p + b * bg->hot_k : vals + lo;

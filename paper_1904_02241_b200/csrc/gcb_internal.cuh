@@ -252,6 +252,12 @@ inline void ensure_smem_attrs(gcb_ctx *ctx, const void *kern, size_t smem, int c
   }
 }
 
+inline int max_smem_optin(gcb_ctx *ctx) {
+  int optin = 0;
+  GCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  return optin;
+}
+
 inline void after_launch(gcb_ctx *ctx, const char *name) {
   ctx->launches++;
   cudaError_t e = cudaGetLastError();

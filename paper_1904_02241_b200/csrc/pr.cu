@@ -453,7 +453,13 @@ __global__ void k_pr_init(int64_t n, double r0, const uint32_t *__restrict__ deg
 // iteration's contributions (185-191) and clearing sums for the next pass.
 // One 4-vertex quad per thread (update_grid): 256-bit loads and stores, the
 // CTA reduces its delta once at the end.  The arithmetic is pr_math.cuh's.
-template <bool EXACT>
+// RANKS = false (tol == 0, every iteration but the last): the intermediate
+// ranks are dead -- the next iteration reads only the contributions, and the
+// L1 delta (kernels.py:399) is compared with tol = 0, which it can never fall
+// below -- so neither the old ranks are read nor the new ones written: 28 B
+// per vertex instead of 44.  The contributions are computed from the same
+// r' = base + d*s, so every result stays bit-identical.
+template <bool EXACT, bool RANKS>
 __global__ void __launch_bounds__(512, 2)
     k_pr_update2(int64_t n, double base, double damping, double *__restrict__ sums,
                  double *__restrict__ ranks, const uint32_t *__restrict__ deg,
@@ -465,7 +471,7 @@ __global__ void __launch_bounds__(512, 2)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint4 *D = reinterpret_cast<const uint4 *>(deg);
   auto store = [&](int64_t i, const double *nr, const double *c) {
-    st_f64x4(ranks + 4 * i, nr[0], nr[1], nr[2], nr[3]);
+    if (RANKS) st_f64x4(ranks + 4 * i, nr[0], nr[1], nr[2], nr[3]);
     st_f64x4(sums + 4 * i, 0.0, 0.0, 0.0, 0.0);
     if (contrib) st_f64x4(contrib + 4 * i, c[0], c[1], c[2], c[3]);
     if (contrib32)
@@ -473,14 +479,18 @@ __global__ void __launch_bounds__(512, 2)
           make_float4(__double2float_rn(c[0]), __double2float_rn(c[1]), __double2float_rn(c[2]),
                       __double2float_rn(c[3]));
   };
+  auto old = [&](int64_t i, double *o) {
+    if (RANKS) ld_rw_f64x4(ranks + 4 * i, o);
+    else o[0] = o[1] = o[2] = o[3] = 0.0;
+  };
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + stride < n4; i += 2 * stride) {
     const int64_t k = i + stride;
     double sa[4], sb[4], oa[4], ob[4], nr[4], c[4];
     ld_rw_f64x4(sums + 4 * i, sa);
     ld_rw_f64x4(sums + 4 * k, sb);
-    ld_rw_f64x4(ranks + 4 * i, oa);
-    ld_rw_f64x4(ranks + 4 * k, ob);
+    old(i, oa);
+    old(k, ob);
     const uint4 da = __ldcs(D + i), db = __ldcs(D + k);
     pr_quad<EXACT>(sa, oa, da, base, damping, nr, c, dsum);
     store(i, nr, c);
@@ -490,19 +500,20 @@ __global__ void __launch_bounds__(512, 2)
   if (i < n4) {
     double sa[4], oa[4], nr[4], c[4];
     ld_rw_f64x4(sums + 4 * i, sa);
-    ld_rw_f64x4(ranks + 4 * i, oa);
+    old(i, oa);
     pr_quad<EXACT>(sa, oa, D[i], base, damping, nr, c, dsum);
     store(i, nr, c);
   }
   for (int64_t v = (n4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
     const double nr = __dadd_rn(base, __dmul_rn(damping, sums[v]));
-    dsum += fabs(nr - ranks[v]);
+    if (RANKS) dsum += fabs(nr - ranks[v]);
     const double c = deg[v] ? div_deg<EXACT>(nr, deg[v]) : 0.0;
-    ranks[v] = nr;
+    if (RANKS) ranks[v] = nr;
     sums[v] = 0.0;
     if (contrib) contrib[v] = c;
     if (contrib32) contrib32[v] = __double2float_rn(c);
   }
+  if (!RANKS) return;
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, d);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dsum;
@@ -523,14 +534,19 @@ static unsigned update_grid(gcb_ctx *ctx, int64_t n) {
 
 static void launch_update(gcb_ctx *ctx, bool exact, int64_t n, double base, double damping,
                           double *sums, double *ranks, const uint32_t *deg, double *contrib,
-                          float *contrib32, double *deltas) {
+                          float *contrib32, double *deltas, bool with_ranks = true) {
   const unsigned g = update_grid(ctx, n);
-  if (exact)
-    k_pr_update2<true><<<g, 512, 0, ctx->stream>>>(n, base, damping, sums, ranks, deg, contrib,
-                                                   contrib32, deltas);
-  else
-    k_pr_update2<false><<<g, 512, 0, ctx->stream>>>(n, base, damping, sums, ranks, deg, contrib,
-                                                    contrib32, deltas);
+#define GCB_UPD(E, R)                                                                           \
+  k_pr_update2<E, R><<<g, 512, 0, ctx->stream>>>(n, base, damping, sums, ranks, deg, contrib,   \
+                                                 contrib32, deltas)
+  if (exact) {
+    if (with_ranks) GCB_UPD(true, true);
+    else GCB_UPD(true, false);
+  } else {
+    if (with_ranks) GCB_UPD(false, true);
+    else GCB_UPD(false, false);
+  }
+#undef GCB_UPD
   after_launch(ctx, "k_pr_update2");
 }
 
@@ -681,6 +697,120 @@ __global__ void __launch_bounds__(1024, 1)
   for (int i = threadIdx.x; i < hot; i += blockDim.x) {
     const double v =
         FIX ? (double)(((unsigned long long)s_hi[i] << 32) | s_lo[i]) * kFixInv : s_acc[i];
+    if (v != 0.0) atomicAdd(sums + hot_ids_b[i], v);
+  }
+}
+
+// The hybrid hub pass (relabel.cu hybrid_split): every edge runs from a cold
+// source into a hub destination, and a cold source has few such edges, so a
+// 256-edge tile spans ~40 source rows on average (rmat:24).  k_push_hot loads
+// the values of a tile's first 32 rows when the tile starts (id_map -> vals,
+// two dependent L2 round trips exposed per tile) and every edge of a later
+// row loads id_map -> vals itself.  Here the row values of the NEXT tile are
+// fetched while this tile's adds run: the tile_row of tile t+2, the id_map
+// words of tile t+1 and then their values are issued one pipeline stage
+// ahead, two rows per lane (the first 64 rows of a tile) held in registers
+// and handed to the edges by shuffle; rows past 64 load directly.  The hub
+// adds use the two-word fixed point of fix_add.
+// the tile loop of k_push_hub (one warp, tiles t, t + stride, ...)
+__device__ __forceinline__ void hub_tiles(
+    const uint32_t *__restrict__ xcol, const uint32_t *__restrict__ rstart,
+    const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0, int64_t ntiles,
+    uint32_t Lb, const uint32_t *__restrict__ id_map_b, const double *__restrict__ vals,
+    double *__restrict__ sums, unsigned *s_lo, unsigned *s_hi, int64_t t, int64_t stride,
+    int lane, uint64_t pol_stream) {
+  constexpr int V = kTileV, T = kTileT;
+  constexpr uint32_t kHot = 0x80000000u;
+  const unsigned FULL = 0xffffffffu;
+  auto row_id = [&](uint32_t r) { return r < Lb ? __ldg(id_map_b + r) : 0u; };
+  // pipeline state: tile t's words and row values, tile t+1's first row
+  uint32_t c[V], fw, r0, r0n = 0;
+  double rvA, rvB;
+  {
+    const int64_t abase = (t0 + t) * T;
+    ld_stream_u32x8(xcol + abase + lane * V, pol_stream, c);
+    fw = rstart[(abase >> 5) + (lane < 8 ? lane : 8)];
+    r0 = tile_row[t];
+    if (t + stride < ntiles) r0n = tile_row[t + stride];
+    rvA = __ldg(vals + row_id(r0 + lane));
+    rvB = __ldg(vals + row_id(r0 + 32 + lane));
+  }
+  for (; t < ntiles; t += stride) {
+    const int64_t abase = (t0 + t) * T;
+    const int64_t tn = t + stride;
+    const bool has_next = tn < ntiles;
+    // stage 1 for tile t+1: its arena words and its rows' ids; tile t+2's first row
+    uint32_t cn[V] = {0, 0, 0, 0, 0, 0, 0, 0}, fwn = 0, r0nn = 0, idA = 0, idB = 0;
+    if (has_next) {
+      const int64_t nb = (t0 + tn) * T;
+      ld_stream_u32x8(xcol + nb + lane * V, pol_stream, cn);
+      fwn = rstart[(nb >> 5) + (lane < 8 ? lane : 8)];
+      if (tn + stride < ntiles) r0nn = tile_row[tn + stride];
+      idA = row_id(r0n + lane);
+      idB = row_id(r0n + 32 + lane);
+    }
+    // this tile's rows
+    const int llo = es > abase ? (int)(es - abase) : 0;
+    const int lhi = ee - abase < T ? (int)(ee - abase) : T;
+    const TileBits tb = tile_bits(fw, llo, lhi, lane);
+    const int cnt = __popc(tb.bits);
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
+    }
+    // stage 2 for tile t+1: the row values (the ids have had the scan's time)
+    double rvAn = 0.0, rvBn = 0.0;
+    if (has_next) {
+      rvAn = __ldg(vals + idA);
+      rvBn = __ldg(vals + idB);
+    }
+    const int kf = tb.vm ? __ffs(tb.vm) - 1 : 0;
+    uint32_t rr = (uint32_t)(incl - cnt) + ((tb.bits >> kf) & 1u);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      if (k > kf && ((tb.bits >> k) & 1u)) ++rr;
+      const double xa = __shfl_sync(FULL, rvA, rr & 31);
+      const double xb = __shfl_sync(FULL, rvB, rr & 31);
+      if (!((tb.vm >> k) & 1u)) continue;
+      const double x = rr < 32 ? xa : (rr < 64 ? xb : __ldg(vals + __ldg(id_map_b + r0 + rr)));
+      if (c[k] & kHot) fix_add(s_lo, s_hi, c[k] & ~kHot, __double2ull_rn(x * kFixScale));
+      else atomicAdd(sums + c[k], x);  // not a hub (cannot happen for hybrid_split edges)
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) c[k] = cn[k];
+    fw = fwn;
+    r0 = r0n;
+    r0n = r0nn;
+    rvA = rvAn;
+    rvB = rvBn;
+  }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+    k_push_hub(const uint32_t *__restrict__ xcol, const uint32_t *__restrict__ rstart,
+               const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
+               int64_t ntiles, uint32_t Lb, const uint32_t *__restrict__ id_map_b,
+               const uint32_t *__restrict__ hot_ids_b, int hot, const double *__restrict__ vals,
+               double *__restrict__ sums) {
+  constexpr int V = kTileV, T = kTileT;
+  constexpr uint32_t kHot = 0x80000000u;
+  extern __shared__ double smem_d[];
+  unsigned *s_lo = reinterpret_cast<unsigned *>(smem_d), *s_hi = s_lo + hot;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t pol_stream = policy_evict_first();
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) smem_d[i] = 0.0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * NW;
+  int64_t t = (int64_t)blockIdx.x * NW + wid;
+  if (t < ntiles) hub_tiles(xcol, rstart, tile_row, es, ee, t0, ntiles, Lb, id_map_b, vals,
+                            sums, s_lo, s_hi, t, stride, lane, pol_stream);
+  __syncthreads();
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) {
+    const double v = (double)(((unsigned long long)s_hi[i] << 32) | s_lo[i]) * kFixInv;
     if (v != 0.0) atomicAdd(sums + hot_ids_b[i], v);
   }
 }
@@ -922,6 +1052,18 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
       ensure_smem_attrs(ctx, (const void *)k_push_hot<false>, smem);
       ensure_smem_attrs(ctx, (const void *)k_push_hot<false, true>, smem);
       const unsigned gh = grid_for(nt * 32, 1024, (int64_t)ctx->num_sms);
+      constexpr int kHubNW = 32;
+      const size_t smem_hub = smem;
+      const char *hv = getenv("GCB_HUB_KERNEL");
+      if (nonneg && !wgt && !getenv("GCB_NO_FIX") && !(hv && hv[0] == '0') &&
+          smem_hub <= (size_t)max_smem_optin(ctx)) {
+        ensure_smem_attrs(ctx, (const void *)k_push_hub<kHubNW>, smem_hub);
+        k_push_hub<kHubNW><<<gh, kHubNW * 32, smem_hub, ctx->stream>>>(
+            bg->xcol.p, bg->rstart.p, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
+            (uint32_t)Lb, bg->id_map.p + rs, bg->hot_ids.p + b * bg->hot_k, hot, vals, sums);
+        after_launch(ctx, "k_push_hub");
+        continue;
+      }
       if (nonneg && !wgt && !getenv("GCB_NO_FIX"))
         k_push_hot<false, true><<<gh, 1024, smem, ctx->stream>>>(
             bg->xcol.p, nullptr, bg->rstart.p, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
@@ -1029,7 +1171,7 @@ static bool pr_graph_loop(gcb_ctx *ctx, gcb_blocked *bg, F &&iterate, const void
         throw 0;
       capturing = true;
       ctx->stream = cs;
-      iterate();
+      iterate(true);  // tol > 0: every iteration needs its delta
       k_pr_check<<<1, 1, 0, cs>>>(h, delta_dev, tol, ng->state.p);
       after_launch(ctx, "k_pr_check");
       ctx->stream = saved;
@@ -1116,8 +1258,10 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
                                                  bg->sums.p);
     after_launch(ctx, "k_pr_init");
   }
-  // one iteration's launches (no host synchronisation: also the graph body)
-  auto iterate = [&]() {
+  // one iteration's launches (no host synchronisation: also the graph body);
+  // with_ranks = false only where the ranks and delta are dead (tol == 0, not
+  // the last iteration: see k_pr_update2)
+  auto iterate = [&](bool with_ranks) {
     if (!push && exact && !bg->cb && bg->B >= 1 && contrib) {
       ProfScope ps(ctx, 0);
       exact_pull_concurrent(ctx, bg, contrib, false, bg->sums.p);
@@ -1137,7 +1281,8 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
     {
       ProfScope ps(ctx, 2);
       launch_update(ctx, exact, n, base, damping, bg->sums.p, ranks_dev, deg,
-                    contrib ? contrib : (push ? bg->contrib.p : nullptr), contrib32, bg->deltas.p);
+                    contrib ? contrib : (push ? bg->contrib.p : nullptr), contrib32, bg->deltas.p,
+                    with_ranks);
     }
     if (tol > 0.0) {
       k_reduce_sum<<<1, 1024, 0, ctx->stream>>>(bg->deltas.p, update_grid(ctx, n), delta_dev);
@@ -1146,8 +1291,10 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   };
   double *hdelta = (double *)ctx->pinned;
   int it = 0, cv = 0;
+  const char *kr = getenv("GCB_KEEP_RANKS");  // 1: full update every iteration (A/B knob)
+  const bool keep_ranks = kr && kr[0] == '1';
   for (int k = 0; k < max_iters; ++k) {
-    iterate();
+    iterate(tol > 0.0 || k == max_iters - 1 || keep_ranks);
     ++it;
     if (tol > 0.0) {
       d2h(ctx, hdelta, delta_dev, 1);
