@@ -59,6 +59,8 @@ def parse_args():
                    help="reference arm: stop timing further calls after this many seconds")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-secondary", action="store_true",
+                   help="skip the other BASELINE configs (SpMV rmat:22, BFS / SSSP / CC rmat:24)")
     return p.parse_args()
 
 
@@ -225,6 +227,10 @@ def workload_config(args, n, m, world):
         "layout": ("steady state: degree-ordered copy with hybrid edge classes, built in the "
                    "untimed warm-up (e2e: hot-bit layout of each freshly uploaded graph)"
                    if world == 1 and not args.exact and not args.f32_values else
+                   "degree-ordered shards: graph renumbered by out-degree on every rank, slabs "
+                   "blocked with the prefix hot set (gcb_shard_blocking)"
+                   if world > 1 and not args.exact and not args.f32_values
+                   and os.environ.get("GCB_SHARD_ORDER", "0") == "1" else
                    "as built by the call path (no promotion)"),
         "iterations_per_step": args.iters, "damping": 0.85, "tol": 0.0,
         "direction": args.direction, "value_dtype": "f32" if args.f32_values else "f64",
@@ -286,9 +292,17 @@ def run_ours(args):
 
         if args.direction != "pull":
             raise SystemExit("multi-GPU PageRank shards the pull direction")
+        # GCB_SHARD_ORDER=1: every rank renumbers the graph by out-degree and
+        # blocks its slab with the global prefix hot set.  Off by default: at
+        # rmat:24, P = 8 the slab-local hot sets of the original numbering ran
+        # every shard step faster (max 0.144 vs 0.149 ms, DESIGN 7)
+        ordered = (not args.exact and not args.f32_values
+                   and os.environ.get("GCB_SHARD_ORDER", "0") == "1")
+        if ordered:
+            src, _perm = parallel.degree_order(src)
         plan = parallel.ShardPlan(parallel.shard_ranges(src.row_offsets, world))
         # width 0: size each shard's blocks from the sources its slab reads
-        engine = parallel.DeviceShard(src, *plan.owned(rank), 0, flags)
+        engine = parallel.DeviceShard(src, *plan.owned(rank), 0, flags, ordered)
         # default: the exchange fused into the rank update over peer memory
         # (csrc/exchange.cu); GCB_EXCHANGE=nccl selects the sparse NCCL
         # all_to_all, which is also the fallback when peer mapping fails
@@ -442,6 +456,11 @@ def run_ours(args):
     if not args.no_e2e and world == 1:
         e2e = run_e2e(args, bg, ctx, stream, flags)
 
+    # ---- the other BASELINE configs, one timing each (not the headline) ----
+    secondary = None
+    if world == 1 and not args.no_secondary and args.scale == 24:
+        secondary = run_secondary(ctx, stream, local)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as orc
@@ -485,7 +504,7 @@ def run_ours(args):
             "data": "synthetic R-MAT generated on device (bit-exact with the reference)",
             "config": cfg,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "parity": parity, "layouts": layouts,
+            "parity": parity, "layouts": layouts, "secondary": secondary,
             "gpu_launches": launches, "clocks": clk,
             "setup_s": round(setup_s, 2),
         }
@@ -581,6 +600,100 @@ def default_layout_rate(ctx, bg, stream, args, flags, value, ms_step):
                                       "promotion at 4096 fast iterations)",
                             "value": round(m * args.iters / (ms / 1e3) / 1e9, 3),
                             "ms_per_step": round(ms, 4), "steps": k}}
+
+
+def run_secondary(ctx, stream, local):
+    """BASELINE configs[1] and [3] (plus CC of configs[4]'s algorithm at
+    rmat:24), each against its SURVEY 8(d) byte model.  SpMV runs on device
+    vectors (CUDA events over 20 calls); BFS / SSSP / CC are public API calls
+    whose numpy results come back inside the call (wall time, median of 3
+    after a warm-up that builds the execution layouts)."""
+    import torch
+
+    import paper_1904_02241_b200 as gcb
+    from paper_1904_02241_b200 import _lib
+
+    peak, _ = measured_hbm_peak()
+    out = {}
+
+    def wall(fn, reps=3):
+        fn()
+        ts = []
+        r = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = fn()
+            ts.append(time.perf_counter() - t0)
+        return r, float(np.median(ts))
+
+    # configs[1]: SpMV pull TOCAB, rmat:22, x = default_rng(42).random(n)
+    gt = gcb.generate_rmat(22, 16, 1, transposed=True)
+    n, m = gt.num_vertices, gt.num_edges
+    bg = gcb.partition_tocab(gt, "pull", 1 << 22)
+    del gt
+    h = bg.device()
+    x = np.random.default_rng(42).random(n)
+    xd = torch.from_numpy(x).to(f"cuda:{local}")
+    yd = torch.empty_like(xd)
+
+    def spmv():
+        _lib.check(ctx._lib.gcb_spmv_blocked_dev(ctx.handle, h.raw, ctypes.c_void_p(xd.data_ptr()),
+                                                 0, ctypes.c_void_p(yd.data_ptr())))
+    for _ in range(3):
+        spmv()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(20):
+        spmv()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    b = 4 * m + 4 * (n + 1) + 16 * n
+    y_exact = gcb.spmv_blocked(bg, x, exact=True)
+    rel = float(np.max(np.abs(yd.cpu().numpy() - y_exact) / np.maximum(np.abs(y_exact), 1e-300)))
+    out["spmv"] = {"config": "BASELINE configs[1]: SpMV pull TOCAB rmat:22:16:1, W=2^22, device x/y",
+                   "ms": round(ms, 4), "gteps": round(m / ms / 1e6, 1),
+                   "algorithmic_bytes": b, "achieved_gbs": round(b / ms / 1e6, 1),
+                   "frac": round(b / ms / 1e6 / peak, 4),
+                   "parity_vs_exact_max_rel": rel}
+    del bg, h, xd, yd
+
+    # configs[3]: BFS and SSSP (integer weights) from the hub, rmat:24; CC
+    g = gcb.generate_rmat(24, 16, 1)
+    n, m = g.num_vertices, g.num_edges
+    deg = g.out_degrees
+    bgt = gcb.partition_tocab(gcb.transpose(g), "pull", 1 << 21)
+    r, t = wall(lambda: gcb.bfs(g, 0, g_blocked=bgt))
+    reached = np.flatnonzero(r.depth != gcb.INF_DEPTH)
+    te = int(deg[reached].sum())
+    b = 4 * te + 8 * n
+    out["bfs"] = {"config": "BASELINE configs[3]: BFS from 0 with the direction switch, rmat:24:16:1",
+                  "ms_api": round(t * 1e3, 3), "gteps": round(te / t / 1e9, 2),
+                  "levels": len(r.levels), "directions": r.directions,
+                  "reached": int(reached.size), "algorithmic_bytes": b,
+                  "frac": round(b / t / 1e9 / peak, 4)}
+    del bgt
+    w = np.random.default_rng(7).integers(1, 256, m).astype(np.float64)
+    gw = gcb.CsrGraph(n, m, g.row_offsets, g.col_indices, w)
+    bgw = gcb.partition_tocab(gcb.transpose(gw), "pull", 1 << 21)
+    r, t = wall(lambda: gcb.sssp(gw, 0, g_blocked=bgw))
+    reached = np.flatnonzero(r.dist != gcb.INF_DIST)
+    te = int(deg[reached].sum())
+    b = 4 * te + 8 * n
+    out["sssp"] = {"config": "BASELINE configs[3]: SSSP from 0, weights default_rng(7) U[1,255], "
+                             "rmat:24:16:1",
+                   "ms_api": round(t * 1e3, 3), "gteps": round(te / t / 1e9, 2),
+                   "rounds": r.rounds, "reached": int(reached.size),
+                   "algorithmic_bytes_per_run": b}
+    del bgw, gw, w
+    r, t = wall(lambda: gcb.cc(g))
+    out["cc"] = {"config": "CC (configs[4]'s algorithm) on rmat:24:16:1", "ms_api": round(t * 1e3, 3),
+                 "gteps": round(m / t / 1e9, 2), "components": int(r.num_components)}
+    del g
+    torch.cuda.synchronize()
+    return out
 
 
 def run_e2e(args, bg, ctx, stream, flags, steps=None):

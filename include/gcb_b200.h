@@ -202,6 +202,25 @@ int gcb_pr_shard_init(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1,
 int gcb_pr_shard_step(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, double damping,
                       uint32_t flags, const uint32_t *deg_dev, double *contrib_dev,
                       double *ranks_dev, double *delta_dev);
+/* Degree-ordered destination shards (parallel.py): gcb_csr_degree_order
+ * renumbers a transpose CSR by descending out-degree (ties: ascending id;
+ * perm_dev[old] = new, uint32[n]) -- the permutation the single-GPU promotion
+ * (relabel.cu) picks -- so all ranks share one numbering.  gcb_shard_blocking
+ * blocks one shard's row slab of that graph (pull, `width`) with the prefix
+ * hot set and, where the cost model says it pays, the hybrid hub-destination
+ * push pass that gcb_pr_shard_step(_p2p) then runs after the pull gather.
+ * Fast mode only (the reference's summation order is that of the original
+ * numbering). */
+int gcb_csr_degree_order(gcb_ctx *ctx, const gcb_csr *gt, uint32_t *perm_dev, gcb_csr **out);
+int gcb_shard_blocking(gcb_ctx *ctx, const gcb_csr *slab, int64_t width, gcb_blocked **out);
+/* The NCCL exchange between gcb_pr_shard_step calls (parallel.SparseExchange,
+ * SURVEY 8e): out[i] = full[idx[i]] packs the values the peers read into the
+ * all_to_all send buffer; full[idx[i]] = in[i] scatters the received ones.
+ * Device pointers, uint32 indices, stream-ordered on the ctx stream. */
+int gcb_index_pack_f64(gcb_ctx *ctx, const double *full_dev, const uint32_t *idx_dev,
+                       int64_t count, double *out_dev);
+int gcb_index_unpack_f64(gcb_ctx *ctx, const double *in_dev, const uint32_t *idx_dev,
+                         int64_t count, double *full_dev);
 /* The same step with the contribution exchange fused into the update over
  * peer memory (csrc/exchange.cu), replacing the NCCL exchange between
  * gcb_pr_shard_step calls.  Buffers come from gcb_ipc_alloc and are mapped in

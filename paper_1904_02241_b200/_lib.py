@@ -65,6 +65,10 @@ SIGNATURES = {
     "gcb_csr_col_counts": ([c_vp, c_vp, c_vp], c_int),
     "gcb_pr_shard_init": ([c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp], c_int),
     "gcb_pr_shard_step": ([c_vp, c_vp, c_i64, c_i64, c_dbl, c_u32, c_vp, c_vp, c_vp, c_vp], c_int),
+    "gcb_csr_degree_order": ([c_vp, c_vp, c_vp, PP], c_int),
+    "gcb_shard_blocking": ([c_vp, c_vp, c_i64, PP], c_int),
+    "gcb_index_pack_f64": ([c_vp, c_vp, c_vp, c_i64, c_vp], c_int),
+    "gcb_index_unpack_f64": ([c_vp, c_vp, c_vp, c_i64, c_vp], c_int),
     "gcb_ipc_alloc": ([c_vp, c_i64, PP, c_vp], c_int),
     "gcb_ipc_free": ([c_vp, c_vp], c_int),
     "gcb_ipc_open": ([c_vp, c_vp, PP], c_int),

@@ -20,8 +20,14 @@ void *device_alloc(size_t bytes) {
   return p;
 }
 
+thread_local cudaStream_t t_free_stream = nullptr;
+
 void device_free(void *p) {
   if (!p) return;
+  if (t_free_stream) {  // StreamOrderedFrees: every user of p ran on that stream
+    cudaFreeAsync(p, t_free_stream);
+    return;
+  }
   cudaDeviceSynchronize();  // what cudaFree implies: no stream still reads p
   cudaFreeAsync(p, cudaStreamLegacy);
 }

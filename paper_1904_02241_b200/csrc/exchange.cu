@@ -168,11 +168,60 @@ static void check_peer_error(gcb_ctx *ctx) {
   }
 }
 
+// The NCCL fallback exchange (parallel.SparseExchange): pack the values the
+// peers read into the all_to_all send buffer, and scatter the received ones
+// into the full vector.  32-bit indices (half the index bytes of torch's
+// int64 index_select / index_copy_), 4 per thread.
+__global__ void k_index_pack(int64_t cnt, const uint32_t *__restrict__ idx,
+                             const double *__restrict__ full, double *__restrict__ out) {
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k < cnt) out[i + k] = __ldg(full + __ldcs(idx + i + k));
+  }
+}
+__global__ void k_index_unpack(int64_t cnt, const uint32_t *__restrict__ idx,
+                               const double *__restrict__ in, double *__restrict__ full) {
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k < cnt) full[__ldcs(idx + i + k)] = __ldcs(in + i + k);
+  }
+}
+
 }  // namespace gcb
 
 using namespace gcb;
 
 extern "C" {
+
+int gcb_index_pack_f64(gcb_ctx *ctx, const double *full_dev, const uint32_t *idx_dev, int64_t count,
+                       double *out_dev) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && (count == 0 || (full_dev && idx_dev && out_dev)), "NULL argument");
+  GCB_REQUIRE(count >= 0, "negative count");
+  if (!count) return GCB_OK;
+  DeviceGuard dg(ctx->device);
+  k_index_pack<<<grid_for((count + 3) / 4, 256, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+      count, idx_dev, full_dev, out_dev);
+  after_launch(ctx, "k_index_pack");
+  GCB_API_END
+}
+
+int gcb_index_unpack_f64(gcb_ctx *ctx, const double *in_dev, const uint32_t *idx_dev, int64_t count,
+                         double *full_dev) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && (count == 0 || (full_dev && idx_dev && in_dev)), "NULL argument");
+  GCB_REQUIRE(count >= 0, "negative count");
+  if (!count) return GCB_OK;
+  DeviceGuard dg(ctx->device);
+  k_index_unpack<<<grid_for((count + 3) / 4, 256, (int64_t)ctx->num_sms * 8), 256, 0,
+                   ctx->stream>>>(count, idx_dev, in_dev, full_dev);
+  after_launch(ctx, "k_index_unpack");
+  GCB_API_END
+}
 
 int gcb_ipc_alloc(gcb_ctx *ctx, int64_t bytes, void **ptr, unsigned char *handle) {
   GCB_API_BEGIN
@@ -279,6 +328,10 @@ int gcb_pr_shard_step_p2p(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1,
                                           peer_timeout_ns(), ctx->peer_err_dev);
   after_launch(ctx, "k_wait_peers");
   pull_sums(ctx, bg, contrib_in, nullptr, false, flags, -1, bg->sums.p, true);
+  if (bg->hybrid) {  // degree-ordered shard (gcb_shard_blocking): hub-destination edges
+    ProfScope ps(ctx, 1);
+    push_scatter(ctx, bg->hybrid, contrib_in, bg->sums.p, false, flags, -1, true);
+  }
   if (cnt) {
     GCB_REQUIRE(need_dev, "NULL need mask");
     ProfScope ps(ctx, 2);

@@ -32,7 +32,10 @@
 // other pull graph the top-`hot` sources by out-degree are recoded in an
 // execution copy of the arena (xcol = 0x80000000 | slot) and their values
 // gathered into hotval once per pass (k_fill_hot).
+#include <cstdio>
 #include <cstdlib>
+#include <memory>
+#include <vector>
 
 #include "gcb_internal.cuh"
 #include "ldst.cuh"
@@ -43,6 +46,7 @@ namespace gcb {
 constexpr int kGWarps = 32;  // warps per CTA (1 CTA per SM)
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kHotBit = 0x80000000u;
+constexpr double kL2KeepMB = 32.0;  // evict_last head of a degree-ordered value slice
 
 // One source value: a hot source from shared memory, everything else from
 // L2 (evict_last keeps the block's value slice resident; no L1 allocation --
@@ -78,13 +82,20 @@ __device__ __forceinline__ double gather_one(const double *vals, uint32_t c, uin
 // ASSIGN: out is all zero before this launch (first block of the pass), so a
 // row that lies inside one tile is stored (out[v] = x) instead of
 // read-modify-written -- no dependent load on the emit path.
+// L2 policy of the cold gathers: mode 0 evict_last over everything; modes 1/2
+// a range policy over the block's value slice (policy_range, ldst.cuh)
+struct RangePolicy {
+  int mode;
+  uint32_t keep, total;
+};
+
 template <bool WGT, bool ASSIGN, bool HOTBIT, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
     k_pull_hot(const uint32_t *__restrict__ col, const double *__restrict__ w,
                const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ id_map_b,
                const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
                int64_t ntiles, uint32_t lo, int hot, uint32_t Lb, const double *__restrict__ hot_src,
-               const double *__restrict__ vals, double *__restrict__ out) {
+               const double *__restrict__ vals, double *__restrict__ out, RangePolicy rp) {
   constexpr int V = kTileV;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -92,7 +103,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
   uint32_t *s_ids = reinterpret_cast<uint32_t *>(smem) + wid * 32;
   double *s_hot = reinterpret_cast<double *>(smem + NW * 32 * sizeof(uint32_t));
   const uint32_t s_hot_addr = (uint32_t)__cvta_generic_to_shared(s_hot);
-  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep =
+      rp.mode ? policy_range(vals + lo, rp.keep, rp.total, rp.mode) : policy_evict_last();
   const unsigned FULL = 0xffffffffu;
   const int64_t stride = (int64_t)gridDim.x * NW;
 
@@ -267,42 +280,162 @@ void ensure_row_bits(gcb_ctx *ctx, gcb_blocked *bg) {
   }
 }
 
+// Hot set of every block from the out-degrees in bg->deg as the stream
+// reaches this point: the top-K sources of block b's range get slots
+// [b*K, b*K + K) and slot_of[source] = slot (slot_of is all ~0 on entry).
+struct HotScratch {
+  DArray<uint32_t> slot_of, k1, k2, v1, v2;
+  HotScratch(int64_t n, int64_t width) : slot_of(n), k1(width), k2(width), v1(width), v2(width) {}
+};
+static void select_hot(gcb_ctx *ctx, gcb_blocked *bg, int64_t K, HotScratch &hs) {
+  GCB_CUDA(cudaMemsetAsync(hs.slot_of.p, 0xff, bg->n * sizeof(uint32_t), ctx->stream));
+  for (int64_t b = 0; b < bg->B; ++b) {
+    const int64_t lo = b * bg->width, hi = (lo + bg->width < bg->n) ? lo + bg->width : bg->n;
+    const int64_t cnt = hi - lo;
+    GCB_CUDA(cudaMemcpyAsync(hs.k1.p, bg->deg.p + lo, cnt * sizeof(uint32_t),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    k_iota_range<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(lo, cnt, hs.v1.p);
+    after_launch(ctx, "k_iota_range");
+    uint32_t *rk = nullptr, *rv = nullptr;
+    cub_sort_pairs_desc_u32_u32(ctx, hs.k1.p, hs.k2.p, hs.v1.p, hs.v2.p, cnt, &rk, &rv);
+    k_pick_hot<<<grid_for(K, 256, 4096), 256, 0, ctx->stream>>>(K, cnt, rk, rv,
+                                                                bg->hot_ids.p + b * K, hs.slot_of.p);
+    after_launch(ctx, "k_pick_hot");
+  }
+}
+
+static void recode_range(gcb_ctx *ctx, gcb_blocked *bg, const uint32_t *slot_of, int64_t off,
+                         int64_t cnt) {
+  if (cnt <= 0) return;
+  k_recode<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(cnt, bg->col.p + off, slot_of,
+                                                               bg->xcol.p + off);
+  after_launch(ctx, "k_recode");
+}
+
+static int64_t pull_hot_slots(gcb_ctx *ctx, const gcb_blocked *bg) {
+  int64_t K = hot_capacity(ctx);
+  if (K > bg->width) K = bg->width;
+  if (bg->m == 0) K = 0;  // nothing to gather: no table (and no recode)
+  return K;
+}
+
+static void alloc_hot_tables(gcb_ctx *ctx, gcb_blocked *bg, int64_t K) {
+  GCB_REQUIRE(bg->n < (int64_t(1) << 31), "hot recode needs vertex ids below 2^31");
+  bg->hot_ids.alloc(bg->B * K);
+  bg->hotval.alloc(bg->B * K);
+  bg->xcol.alloc(bg->m + kColPad);
+  GCB_CUDA(cudaMemsetAsync(bg->xcol.p + bg->m, 0, kColPad * sizeof(uint32_t), ctx->stream));
+}
+
 // Row-start bitmap + (non-degree-ordered graphs) hot recode.  Built once.
 void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg) {
   ensure_derived(ctx, bg);
   if (bg->xready) return;
-  const int64_t B = bg->B, n = bg->n;
   ensure_row_bits(ctx, bg);
-  int64_t K = hot_capacity(ctx);
-  if (K > bg->width) K = bg->width;
-  if (bg->m == 0) K = 0;  // nothing to gather: no table (and no recode)
+  const int64_t K = pull_hot_slots(ctx, bg);
   bg->hot_k = K;
   if (!bg->is_relabeled && K > 0) {
-    GCB_REQUIRE(n < (int64_t(1) << 31), "hot recode needs vertex ids below 2^31");
-    bg->hot_ids.alloc(B * K);
-    bg->hotval.alloc(B * K);
-    DArray<uint32_t> slot_of(n), k1(bg->width), k2(bg->width), v1(bg->width), v2(bg->width);
-    GCB_CUDA(cudaMemsetAsync(slot_of.p, 0xff, n * sizeof(uint32_t), ctx->stream));
-    for (int64_t b = 0; b < B; ++b) {
-      const int64_t lo = b * bg->width, hi = (lo + bg->width < n) ? lo + bg->width : n;
-      const int64_t cnt = hi - lo;
-      GCB_CUDA(cudaMemcpyAsync(k1.p, bg->deg.p + lo, cnt * sizeof(uint32_t),
-                               cudaMemcpyDeviceToDevice, ctx->stream));
-      k_iota_range<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(lo, cnt, v1.p);
-      after_launch(ctx, "k_iota_range");
-      uint32_t *rk = nullptr, *rv = nullptr;
-      cub_sort_pairs_desc_u32_u32(ctx, k1.p, k2.p, v1.p, v2.p, cnt, &rk, &rv);
-      k_pick_hot<<<grid_for(K, 256, 4096), 256, 0, ctx->stream>>>(K, cnt, rk, rv,
-                                                                  bg->hot_ids.p + b * K, slot_of.p);
-      after_launch(ctx, "k_pick_hot");
-    }
-    bg->xcol.alloc(bg->m + kColPad);
-    GCB_CUDA(cudaMemsetAsync(bg->xcol.p + bg->m, 0, kColPad * sizeof(uint32_t), ctx->stream));
-    k_recode<<<grid_for(bg->m, 256, 65536), 256, 0, ctx->stream>>>(bg->m, bg->col.p, slot_of.p,
-                                                                   bg->xcol.p);
-    after_launch(ctx, "k_recode");
+    alloc_hot_tables(ctx, bg, K);
+    HotScratch hs(bg->n, bg->width);
+    select_hot(ctx, bg, K, hs);
+    recode_range(ctx, bg, hs.slot_of.p, 0, bg->m);
   }
   sync(ctx);
+  bg->xready = true;
+}
+
+// The col arena of a pull TOCAB blocking from pinned host memory, with the
+// whole execution layout built under the transfer (gcb_blocked_upload).
+// The copy is ~20 ms at rmat:24 (1.07 GB over PCIe), the layout build ~3 ms
+// after it (tile tables, row-start bitmap, per-block hot-set sort, recode),
+// and the out-degree count needs every edge.  So:
+//   * col goes over in chunks on the copy stream, each block's chunks in an
+//     order that sends a strided sample (every 4th chunk of every block) first;
+//   * the tile tables and the row-start bitmap (they need lro only) run while
+//     the first chunks are in flight;
+//   * each chunk's out-degrees are counted as it lands; once the sample has
+//     landed the hot set of every block is picked from the sampled degrees,
+//     and from then on each chunk is recoded as it lands.
+// The hot set only decides which loads are served from shared memory: the
+// ranks are the same for any hot set (the gather's add order does not depend
+// on it).  With fewer than 8 chunks there is no sample: the hot set is picked
+// from the exact degrees after the last chunk, as ensure_exec does.
+void upload_col_overlapped(gcb_ctx *ctx, gcb_blocked *bg, const uint32_t *col_host) {
+  const int64_t n = bg->n, m = bg->m;
+  if (!ctx->copy_stream)
+    GCB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  int64_t chunk = int64_t(16) << 20;  // 64 MB of col per copy
+  if (const char *e = getenv("GCB_UPLOAD_CHUNK")) chunk = atoll(e) > 0 ? atoll(e) : chunk;
+  // chunk list: block by block; the sample (every 4th chunk of each block,
+  // its first included) goes first
+  struct Piece { int64_t off, cnt; };
+  std::vector<Piece> sample, rest;
+  int64_t total = 0;
+  for (int64_t b = 0; b < bg->B; ++b) {
+    const int64_t es = bg->h_edge_starts[b], ee = bg->h_edge_starts[b + 1];
+    for (int64_t off = es, j = 0; off < ee; off += chunk, ++j) {
+      const Piece pc{off, ee - off < chunk ? ee - off : chunk};
+      (j % 4 == 0 ? sample : rest).push_back(pc);
+      ++total;
+    }
+  }
+  if (total < 8) {  // small upload: exact degrees, no sample
+    for (const Piece &pc : sample) rest.push_back(pc);
+    sample.clear();
+  }
+  std::vector<Piece> order(sample);
+  order.insert(order.end(), rest.begin(), rest.end());
+
+  // every allocation before the first copy is queued (an allocation waits for
+  // the legacy stream; frees below are stream-ordered)
+  bg->deg.alloc(n);
+  GCB_CUDA(cudaMemsetAsync(bg->deg.p, 0, (n ? n : 1) * sizeof(uint32_t), ctx->stream));
+  const int64_t K = pull_hot_slots(ctx, bg);
+  const bool recode = K > 0;
+  std::unique_ptr<HotScratch> hs;
+  if (recode) {
+    alloc_hot_tables(ctx, bg, K);
+    hs.reset(new HotScratch(n, bg->width));
+  }
+  bg->deg_ready = true;  // counted below, in stream order
+  {
+    cudaEvent_t ready;
+    GCB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    GCB_CUDA(cudaEventRecord(ready, ctx->stream));
+    GCB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
+    cudaEventDestroy(ready);
+  }
+  std::vector<cudaEvent_t> landed(order.size());
+  for (size_t i = 0; i < order.size(); ++i) {
+    GCB_CUDA(cudaMemcpyAsync(bg->col.p + order[i].off, col_host + order[i].off,
+                             order[i].cnt * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                             ctx->copy_stream));
+    GCB_CUDA(cudaEventCreateWithFlags(&landed[i], cudaEventDisableTiming));
+    GCB_CUDA(cudaEventRecord(landed[i], ctx->copy_stream));
+  }
+  StreamOrderedFrees frees(ctx->stream);
+  ensure_derived(ctx, bg);   // tile tables: lro only (its syncs wait for this stream alone)
+  ensure_row_bits(ctx, bg);
+  auto count = [&](size_t i) {
+    GCB_CUDA(cudaStreamWaitEvent(ctx->stream, landed[i], 0));
+    cudaEventDestroy(landed[i]);  // released once the wait is satisfied
+    k_deg_count(ctx, order[i].cnt, bg->col.p + order[i].off, bg->deg.p);
+  };
+  for (size_t i = 0; i < sample.size(); ++i) count(i);
+  if (recode && !sample.empty()) {
+    select_hot(ctx, bg, K, *hs);
+    for (size_t i = 0; i < sample.size(); ++i) recode_range(ctx, bg, hs->slot_of.p, order[i].off, order[i].cnt);
+  }
+  for (size_t i = sample.size(); i < order.size(); ++i) {
+    count(i);
+    if (recode && !sample.empty()) recode_range(ctx, bg, hs->slot_of.p, order[i].off, order[i].cnt);
+  }
+  if (recode && sample.empty()) {
+    select_hot(ctx, bg, K, *hs);
+    recode_range(ctx, bg, hs->slot_of.p, 0, m);
+  }
+  bg->hot_k = K;
+  hs.reset();
   bg->xready = true;
 }
 
@@ -374,11 +507,37 @@ static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double 
   int64_t grid = ceil_div(nt, kGWarps);
   if (grid > ctx->num_sms) grid = ctx->num_sms;
   const double *hot_src = HOTBIT ? bg->hotval.p + b * bg->hot_k : vals + lo;
+  // L2 residency window of the cold gathers (north star (1)): on the
+  // degree-ordered copy the block's value slice is sorted by out-degree, so
+  // its head holds the most-read cold values.  A range policy -- the
+  // per-instruction form of an access-policy window (createpolicy.range) --
+  // marks the first kL2KeepMB of the slice evict_last and leaves the tail at
+  // normal priority; at rmat:24 (64 MB slices) that ran 8.597 vs 8.610 ms per
+  // step against evict_last over the whole slice, and beat the launch-attribute
+  // window with a persisting set-aside (which carves L2 from every other
+  // pass, profiles/r1b_l2_policy.txt).  Marking the tail evict_first instead
+  // ran 8.650 ms; a 16 MB window 9.08 ms (profiles/r2_l2_window.txt).
+  // GCB_L2_RANGE="<MB>:<mode>" overrides (mode 1: tail evict_first, 2: tail
+  // unchanged, 0: whole slice evict_last); the hot-bit layout has no sorted
+  // slice and keeps evict_last.
+  RangePolicy rp{0, 0, 0};
+  {
+    double mb = kL2KeepMB;
+    int mode = HOTBIT ? 0 : 2;
+    if (const char *e = getenv("GCB_L2_RANGE")) {
+      if (sscanf(e, "%lf:%d", &mb, &mode) != 2 || mode < 0 || mode > 2) mode = 0;
+    }
+    const uint64_t total = (uint64_t)(hi - lo) * 8u;
+    uint64_t keep = (uint64_t)(mb * 1048576.0);
+    if (keep > total) keep = total;
+    if (mode && keep < total && total < (uint64_t(1) << 32))
+      rp = RangePolicy{mode, (uint32_t)keep, (uint32_t)total};
+  }
   k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps>
       <<<(unsigned)(grid < 1 ? 1 : grid), kGWarps * 32, smem, ctx->stream>>>(
           HOTBIT ? bg->xcol.p : bg->col.p, WGT ? bg->w.p : nullptr, bg->rstart.p,
           bg->id_map.p + rs, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt, (uint32_t)lo, hot,
-          (uint32_t)Lb, hot_src, vals, out);
+          (uint32_t)Lb, hot_src, vals, out, rp);
   after_launch(ctx, "k_pull_hot");
 }
 

@@ -60,6 +60,16 @@ int set_last_error(int code, const char *msg);
 // ---------------------------------------------------------------------------
 void *device_alloc(size_t bytes);   // ctx.cu
 void device_free(void *p);          // ctx.cu
+// While one is alive, device_free on this thread is stream-ordered on `s`
+// instead of a device-wide synchronisation: for code whose temporaries are
+// only touched by kernels on `s` and that must not stall the host behind
+// copies queued on another stream (the overlapped upload, partition.cu).
+extern thread_local cudaStream_t t_free_stream;
+struct StreamOrderedFrees {
+  cudaStream_t prev;
+  explicit StreamOrderedFrees(cudaStream_t s) : prev(t_free_stream) { t_free_stream = s; }
+  ~StreamOrderedFrees() { t_free_stream = prev; }
+};
 
 template <typename T>
 struct DArray {
@@ -319,6 +329,7 @@ int bits_for(int64_t n);
 // partition.cu
 gcb_blocked *partition_device(gcb_ctx *ctx, const gcb_csr *g, int direction, int64_t width);
 void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg);
+void k_deg_count(gcb_ctx *ctx, int64_t cnt, const uint32_t *col, uint32_t *deg);  // out-degree += per source
 gcb_blocked *csr_compact_view(gcb_ctx *ctx, gcb_csr *g);
 void compute_range_bounds(gcb_ctx *ctx, const gcb_blocked *bg, int64_t k, int64_t *bounds_dev);
 // value kernels (pr.cu)
@@ -327,6 +338,7 @@ void pull_sums(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, const float *v
 void merge_to(gcb_ctx *ctx, gcb_blocked *bg, double *out);
 // gather.cu: fast pull gather accumulating into a dense vector (hot staging)
 void ensure_exec(gcb_ctx *ctx, gcb_blocked *bg);
+void upload_col_overlapped(gcb_ctx *ctx, gcb_blocked *bg, const uint32_t *col_host);
 void ensure_row_bits(gcb_ctx *ctx, gcb_blocked *bg);  // rstart only (tiles.cuh kernels)
 void ensure_long_rows(gcb_ctx *ctx, gcb_blocked *bg);  // exact pull's long-row lists
 void ensure_push_exec(gcb_ctx *ctx, gcb_blocked *bg, int64_t hot_slots);  // push hot destinations

@@ -24,6 +24,22 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// Range policy (the per-instruction form of an access-policy window):
+// evict_last for [base, base + keep), the secondary priority for
+// [base + keep, base + total) -- mode 1: evict_first, mode 2: evict_unchanged.
+__device__ __forceinline__ uint64_t policy_range(const void *base, uint32_t keep, uint32_t total,
+                                                 int mode) {
+  uint64_t p;
+  if (mode == 1)
+    asm("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+        : "=l"(p)
+        : "l"(base), "r"(keep), "r"(total));
+  else
+    asm("createpolicy.range.global.L2::evict_last.L2::evict_unchanged.b64 %0, [%1], %2, %3;"
+        : "=l"(p)
+        : "l"(base), "r"(keep), "r"(total));
+  return p;
+}
 __device__ __forceinline__ uint4 ld_stream_u4(const void *ptr, uint64_t pol) {
   uint4 r;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"

@@ -188,6 +188,12 @@ __global__ void k_deg_pull(int64_t m, const uint32_t *__restrict__ col, uint32_t
     atomicAdd(&deg[col[i]], 1u);
 }
 
+void k_deg_count(gcb_ctx *ctx, int64_t cnt, const uint32_t *col, uint32_t *deg) {
+  if (cnt <= 0) return;
+  k_deg_pull<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(cnt, col, deg);
+  after_launch(ctx, "k_deg_pull");
+}
+
 __global__ void k_deg_push(int64_t B, const int64_t *__restrict__ row_starts,
                            const uint32_t *__restrict__ lro, const uint32_t *__restrict__ id_map,
                            int64_t L, uint32_t *__restrict__ deg) {
@@ -750,40 +756,19 @@ int gcb_blocked_upload(gcb_ctx *ctx, int direction, int64_t width, int64_t n, in
       GCB_REQUIRE(hbad == 0, "local row offset out of the 32-bit range");
     }
     h2d(ctx, bg->id_map.p, id_map_host, L);
-    // col (the bulk of the bytes): for a pull blocking from pinned memory the
-    // copy is chunked on a second stream and the out-degree count
-    // (kernels.py:324-330) runs on each chunk as it lands, hidden behind the
-    // transfer (2.9 ms of the e2e step at rmat:24 otherwise)
+    // col (the bulk of the bytes): from pinned memory, a pull blocking's copy is
+    // chunked on a second stream and the out-degree count plus the whole fast
+    // execution layout are built under it (gather.cu upload_col_overlapped).
+    // Not for a blocking shaped like the cb scheme (every block holds all n
+    // rows): gcb_blocked_mark_cb may still follow, before anything is derived.
     cudaPointerAttributes pa;
     const bool pinned_col = m > 0 && cudaPointerGetAttributes(&pa, col_arena_host) == cudaSuccess &&
                             pa.type == cudaMemoryTypeHost;
     (void)cudaGetLastError();
-    if (direction == 0 && pinned_col && !bg->cb) {
-      if (!ctx->copy_stream)
-        GCB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-      bg->deg.alloc(n);
-      GCB_CUDA(cudaMemsetAsync(bg->deg.p, 0, (n ? n : 1) * sizeof(uint32_t), ctx->stream));
-      // the copy stream starts after the allocations / memsets above
-      cudaEvent_t ready;
-      GCB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-      GCB_CUDA(cudaEventRecord(ready, ctx->stream));
-      GCB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
-      cudaEventDestroy(ready);
-      const int64_t chunk = int64_t(16) << 20;  // 64 MB of col per step
-      for (int64_t off = 0; off < m; off += chunk) {
-        const int64_t cnt = m - off < chunk ? m - off : chunk;
-        GCB_CUDA(cudaMemcpyAsync(bg->col.p + off, col_arena_host + off, cnt * sizeof(uint32_t),
-                                 cudaMemcpyHostToDevice, ctx->copy_stream));
-        cudaEvent_t ev;
-        GCB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        GCB_CUDA(cudaEventRecord(ev, ctx->copy_stream));
-        GCB_CUDA(cudaStreamWaitEvent(ctx->stream, ev, 0));
-        cudaEventDestroy(ev);  // released once the wait is satisfied
-        k_deg_pull<<<grid_for(cnt, 256, 65536), 256, 0, ctx->stream>>>(cnt, bg->col.p + off,
-                                                                       bg->deg.p);
-        after_launch(ctx, "k_deg_pull");
-      }
-      bg->deg_ready = true;
+    bool cb_shaped = B > 0;
+    for (int64_t b = 0; b <= B && cb_shaped; ++b) cb_shaped = bg->h_row_starts[b] == b * n;
+    if (direction == 0 && pinned_col && !cb_shaped) {
+      upload_col_overlapped(ctx, bg, col_arena_host);
     } else {
       h2d(ctx, bg->col.p, col_arena_host, m);
     }

@@ -1604,6 +1604,10 @@ int gcb_pr_shard_step(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, dou
   // gather reads the full contribution vector, then the owned slice is
   // updated in place (stream order keeps the two phases apart)
   pull_sums(ctx, bg, contrib_dev, nullptr, false, flags, -1, bg->sums.p, true);
+  if (bg->hybrid) {  // degree-ordered shard (gcb_shard_blocking): hub-destination edges
+    ProfScope ps(ctx, 1);
+    push_scatter(ctx, bg->hybrid, contrib_dev, bg->sums.p, false, flags, -1, true);
+  }
   if (cnt) {
     ProfScope ps(ctx, 2);
     launch_update(ctx, flags & GCB_FLAG_EXACT, cnt, (1.0 - damping) / (double)bg->n, damping,

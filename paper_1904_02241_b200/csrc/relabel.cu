@@ -175,13 +175,13 @@ __global__ void k_split_edges(int64_t m, const uint32_t *__restrict__ flag, cons
 
 // rows/cols (renumbered transpose edges, in place) keep the pull edges;
 // returns their count and the push CSR of the split-off edges
-int64_t hybrid_split(gcb_ctx *ctx, gcb_blocked *bg, DArray<uint32_t> &rows, DArray<uint32_t> &cols,
-                     const double *w, DArray<double> &w_pull, gcb_csr **push_csr) {
-  const int64_t n = bg->n, m = bg->m;
+static int64_t hybrid_split(gcb_ctx *ctx, int64_t n, int64_t m, int64_t width,
+                            DArray<uint32_t> &rows, DArray<uint32_t> &cols, const double *w,
+                            DArray<double> &w_pull, gcb_csr **push_csr) {
   *push_csr = nullptr;
   const int64_t hs = hot_capacity(ctx);
   const int64_t hd = hybrid_hub_slots(ctx);
-  if (hs <= 0 || hd <= 0 || bg->width <= hs) return m;  // whole slices are hot already
+  if (m == 0 || hs <= 0 || hd <= 0 || width <= hs) return m;  // whole slices are hot already
   DArray<uint8_t> hot_dst(n);
   {
     DArray<uint32_t> k1(n), k2(n), v1(n), v2(n);
@@ -198,7 +198,7 @@ int64_t hybrid_split(gcb_ctx *ctx, gcb_blocked *bg, DArray<uint32_t> &rows, DArr
     after_launch(ctx, "k_mark_top");
   }
   DArray<uint32_t> flag(m + 1), pos(m + 1);
-  k_class_b<<<grid_for(m, 256, 65536), 256, 0, ctx->stream>>>(m, rows.p, cols.p, bg->width,
+  k_class_b<<<grid_for(m, 256, 65536), 256, 0, ctx->stream>>>(m, rows.p, cols.p, width,
                                                              (uint32_t)hs, hot_dst.p, flag.p);
   after_launch(ctx, "k_class_b");
   GCB_CUDA(cudaMemsetAsync(flag.p + m, 0, sizeof(uint32_t), ctx->stream));
@@ -321,7 +321,7 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
     const double *w = bg->weighted ? bg->w.p : nullptr;
     DArray<double> wpull;
     if (hybrid_enabled()) {
-      m_pull = hybrid_split(ctx, bg, rows, cols, w, wpull, &push_csr);
+      m_pull = hybrid_split(ctx, n, m, bg->width, rows, cols, w, wpull, &push_csr);
       if (push_csr && bg->weighted) w = wpull.p;  // split: the pull edges' own weights
     }
     try {
@@ -373,3 +373,128 @@ void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, doubl
 }
 
 }  // namespace gcb
+
+// ---------------------------------------------------------------------------
+// Degree-ordered destination shards (parallel.py).  A shard cannot
+// promote itself the way ensure_relabeled does: every rank's contribution
+// vector must use one numbering.  So the whole transpose is renumbered once
+// (gcb_csr_degree_order, the permutation ensure_relabeled would pick from the
+// global out-degrees), the shards are contiguous row ranges of the renumbered
+// graph, and each shard's slab is blocked with the prefix hot set (and, where
+// the cost model says it pays, the hybrid hub-destination push pass) by
+// gcb_shard_blocking.
+// ---------------------------------------------------------------------------
+namespace gcb {
+
+__global__ void k_csr_edges(int64_t n, const int64_t *__restrict__ ro, const uint32_t *__restrict__ col,
+                            const uint32_t *__restrict__ perm, uint32_t *__restrict__ rows_out,
+                            uint32_t *__restrict__ cols_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const int64_t s = ro[r], e = ro[r + 1];
+    const uint32_t d = perm ? perm[r] : (uint32_t)r;
+    for (int64_t i = s + lane; i < e; i += 32) {
+      rows_out[i] = d;
+      cols_out[i] = perm ? perm[col[i]] : col[i];
+    }
+  }
+}
+
+static void csr_edge_list(gcb_ctx *ctx, const gcb_csr *g, const uint32_t *perm, uint32_t *rows,
+                          uint32_t *cols) {
+  if (!g->m) return;
+  k_csr_edges<<<grid_for(g->n * 32, 256, 65536), 256, 0, ctx->stream>>>(g->n, g->ro.p, g->col.p, perm,
+                                                                       rows, cols);
+  after_launch(ctx, "k_csr_edges");
+}
+
+}  // namespace gcb
+
+using namespace gcb;
+
+extern "C" {
+
+int gcb_csr_degree_order(gcb_ctx *ctx, const gcb_csr *gt, uint32_t *perm_dev, gcb_csr **out) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && gt && perm_dev && out, "NULL argument");
+  GCB_REQUIRE(gt->n < (int64_t(1) << 32), "vertex count exceeds the 32-bit id space");
+  DeviceGuard dg(ctx->device);
+  const int64_t n = gt->n, m = gt->m;
+  {
+    // out-degree of every source = its count among the transpose's columns;
+    // stable sort (deg desc, id asc) as ensure_relabeled
+    DArray<uint32_t> k1(n), k2(n), v1(n), v2(n);
+    GCB_CUDA(cudaMemsetAsync(k1.p, 0, (n ? n : 1) * sizeof(uint32_t), ctx->stream));
+    if (m) {
+      k_count_u32<<<grid_for(m, 256, 65536), 256, 0, ctx->stream>>>(m, gt->col.p, k1.p);
+      after_launch(ctx, "k_count_u32");
+    }
+    if (n) {
+      k_iota_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, v1.p);
+      after_launch(ctx, "k_iota_u32");
+      uint32_t *rk = nullptr, *inv = nullptr;
+      cub_sort_pairs_desc_u32_u32(ctx, k1.p, k2.p, v1.p, v2.p, n, &rk, &inv);
+      k_invert<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, inv, perm_dev);
+      after_launch(ctx, "k_invert");
+    }
+  }
+  DArray<uint32_t> rows(m ? m : 1), cols(m ? m : 1);
+  csr_edge_list(ctx, gt, perm_dev, rows.p, cols.p);
+  DArray<double> w;
+  if (gt->weighted && m) {
+    // weights follow their edge: carried through the builder's sort
+    w.alloc(m);
+    GCB_CUDA(cudaMemcpyAsync(w.p, gt->w.p, m * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  }
+  *out = csr_from_device_edges(ctx, n, m, rows.p, cols.p, gt->weighted ? w.p : nullptr);
+  sync(ctx);
+  GCB_API_END
+}
+
+int gcb_shard_blocking(gcb_ctx *ctx, const gcb_csr *slab, int64_t width, gcb_blocked **out) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && slab && out, "NULL argument");
+  GCB_REQUIRE(width >= 1, "width must be >= 1");
+  DeviceGuard dg(ctx->device);
+  const int64_t n = slab->n, m = slab->m;
+  gcb_csr *pull_csr = nullptr, *push_csr = nullptr;
+  if (hybrid_enabled() && m > 0) {
+    DArray<uint32_t> rows(m), cols(m);
+    csr_edge_list(ctx, slab, nullptr, rows.p, cols.p);
+    DArray<double> wpull;
+    const int64_t mp = hybrid_split(ctx, n, m, width, rows, cols,
+                                    slab->weighted ? slab->w.p : nullptr, wpull, &push_csr);
+    if (push_csr) {
+      try {
+        pull_csr = csr_from_device_edges(ctx, n, mp, rows.p, cols.p,
+                                         slab->weighted ? wpull.p : nullptr);
+      } catch (...) {
+        gcb_csr_destroy(push_csr);
+        throw;
+      }
+    }
+  }
+  gcb_blocked *bg = nullptr;
+  try {
+    bg = partition_device(ctx, pull_csr ? pull_csr : slab, 0, width);
+    bg->is_relabeled = true;  // sources are in degree order: prefix hot set, no recode
+    if (push_csr) {
+      bg->hybrid = partition_device(ctx, push_csr, 1, n);  // one block: every hub slot
+      ensure_push_exec(ctx, bg->hybrid, hybrid_hub_slots(ctx));
+    }
+  } catch (...) {
+    delete bg;
+    if (pull_csr) gcb_csr_destroy(pull_csr);
+    if (push_csr) gcb_csr_destroy(push_csr);
+    throw;
+  }
+  if (pull_csr) gcb_csr_destroy(pull_csr);
+  if (push_csr) gcb_csr_destroy(push_csr);
+  sync(ctx);
+  *out = bg;
+  GCB_API_END
+}
+
+}  // extern "C"

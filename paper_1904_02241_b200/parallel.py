@@ -31,7 +31,7 @@ from .blocking import BlockedGraph, partition_tocab
 from .graph import CsrGraph
 from .kernels import PrParams, PrResult
 
-__all__ = ["shard_ranges", "DeviceShard", "TorchExchange", "SparseExchange", "PeerExchange",
+__all__ = ["shard_ranges", "degree_order", "unpermute", "DeviceShard", "TorchExchange", "SparseExchange", "PeerExchange",
            "LoopbackExchange", "ShardedPageRank", "ShardedSpmv", "sharded_pagerank_virtual",
            "sharded_spmv_virtual"]
 
@@ -185,6 +185,21 @@ class SparseExchange:
         import torch.distributed as dist
 
         send, recv = self._buffers(full)
+        if full.is_cuda:  # pack / unpack kernels (csrc/exchange.cu) on the library stream
+            ctx = _lib.context(full.device.index)
+            if not hasattr(self, "_idx32"):
+                self._idx32 = (self.send_idx.to(torch.int32), self.recv_idx.to(torch.int32))
+            s32, r32 = self._idx32
+            _lib.check(ctx._lib.gcb_index_pack_f64(
+                ctx.handle, ctypes.c_void_p(full.data_ptr()), ctypes.c_void_p(s32.data_ptr()),
+                s32.numel(), ctypes.c_void_p(send.data_ptr())), "exchange pack")
+            dist.all_to_all_single(recv, send, output_split_sizes=self.recv_splits,
+                                   input_split_sizes=self.send_splits, group=self.group)
+            _lib.check(ctx._lib.gcb_index_unpack_f64(
+                ctx.handle, ctypes.c_void_p(recv.data_ptr()), ctypes.c_void_p(r32.data_ptr()),
+                r32.numel(), ctypes.c_void_p(full.data_ptr())), "exchange unpack")
+            return
+        # gloo over host tensors (the CPU tests' oracle engine)
         torch.index_select(full, 0, self.send_idx, out=send)
         dist.all_to_all_single(recv, send, output_split_sizes=self.recv_splits,
                                input_split_sizes=self.send_splits, group=self.group)
@@ -343,10 +358,40 @@ class LoopbackExchange:
                     dst[a:b].copy_(src[a:b])
 
 
-class DeviceShard:
-    """One rank's slab of the transpose, TOCAB-blocked, on its GPU."""
+def degree_order(gt: CsrGraph):
+    """The transpose renumbered by descending out-degree (ties: ascending id),
+    on the device: (renumbered CsrGraph, perm) with perm[old id] = new id
+    (int32 tensor on the device).  Every rank renumbers the same graph the same
+    way, so shards of the result share one numbering; ranks come back with
+    ``unpermute``.  The single-GPU promotion (csrc/relabel.cu) picks the same
+    permutation."""
+    import torch
 
-    def __init__(self, gt: CsrGraph, v0: int, v1: int, width: int, flags: int = 0):
+    h = gt.device()
+    ctx = h.ctx
+    perm = torch.empty(max(gt.num_vertices, 1), dtype=torch.int32,
+                       device=torch.device("cuda", ctx.device))
+    raw = ctypes.c_void_p()
+    _lib.check(ctx._lib.gcb_csr_degree_order(ctx.handle, h.raw, ctypes.c_void_p(perm.data_ptr()),
+                                             ctypes.byref(raw)), "degree order")
+    return CsrGraph._from_device(ctx, raw), perm[:gt.num_vertices]
+
+
+def unpermute(values_new, perm):
+    """values in the original numbering: out[v] = values_new[perm[v]]."""
+    return values_new[perm.long()]
+
+
+class DeviceShard:
+    """One rank's slab of the transpose, TOCAB-blocked, on its GPU.
+
+    ``degree_ordered``: ``gt`` is ``degree_order(...)[0]`` -- the slab is then
+    blocked by gcb_shard_blocking (prefix hot set, hybrid hub pass where it
+    pays), the multi-GPU counterpart of the single-GPU promotion.  Fast mode
+    only."""
+
+    def __init__(self, gt: CsrGraph, v0: int, v1: int, width: int, flags: int = 0,
+                 degree_ordered: bool = False):
         import torch
 
         h = gt.device()
@@ -363,7 +408,16 @@ class DeviceShard:
         self.m_local = slab.num_edges
         if width <= 0:
             width = self._auto_width(slab)
-        self.bg: BlockedGraph = partition_tocab(slab, "pull", width)
+        if degree_ordered:
+            if flags & _lib.FLAG_EXACT:
+                raise ValueError("degree-ordered shards run the fast mode only")
+            braw = ctypes.c_void_p()
+            _lib.check(ctx._lib.gcb_shard_blocking(ctx.handle, slab.device().raw, int(width),
+                                                   ctypes.byref(braw)), "shard blocking")
+            self.bg = BlockedGraph._from_device(ctx, braw)
+        else:
+            self.bg: BlockedGraph = partition_tocab(slab, "pull", width)
+        self.degree_ordered = bool(degree_ordered)
         del slab
         dev = torch.device("cuda", ctx.device)
         self.deg = torch.empty(self.n, dtype=torch.int32, device=dev)
@@ -548,14 +602,20 @@ def sharded_spmv_virtual(gt: CsrGraph, x, parts: int, width: int, exact: bool = 
 
 
 def sharded_pagerank_virtual(gt: CsrGraph, parts: int, width: int,
-                             params: PrParams = PrParams(), exact: bool = False) -> PrResult:
+                             params: PrParams = PrParams(), exact: bool = False,
+                             degree_ordered: bool = False) -> PrResult:
     """Run ``parts`` destination shards in lockstep on one GPU with loopback
-    exchange -- the single-device check of the multi-GPU algorithm."""
+    exchange -- the single-device check of the multi-GPU algorithm
+    (``degree_ordered``: on the renumbered graph, ranks permuted back)."""
     import torch
 
+    perm = None
+    if degree_ordered:
+        gt, perm = degree_order(gt)
     plan = ShardPlan(shard_ranges(gt.row_offsets, parts))
     flags = _lib.FLAG_EXACT if exact else 0
-    shards = [DeviceShard(gt, *plan.owned(r), width, flags) for r in range(parts)]
+    shards = [DeviceShard(gt, *plan.owned(r), width, flags, degree_ordered)
+              for r in range(parts)]
     n = gt.num_vertices
     dev = shards[0].device
     contribs = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(parts)]
@@ -574,5 +634,6 @@ def sharded_pagerank_virtual(gt: CsrGraph, parts: int, width: int,
             conv = True
             break
     ex.sync_all(ranks)
+    out = ranks[0] if perm is None else unpermute(ranks[0], perm)
     torch.cuda.synchronize(dev)
-    return PrResult(ranks[0].cpu().numpy(), it, conv)
+    return PrResult(out.cpu().numpy(), it, conv)

@@ -21,8 +21,11 @@ width = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 0 = auto (DeviceShard)
 gt = gcb.generate_rmat(scale, 16, 1, transposed=True)
 n, m = gt.num_vertices, gt.num_edges
 vc = float(os.environ.get('VC', parallel.VERTEX_COST))
+DO = os.environ.get("DO", "0") == "1"  # degree-ordered shards (gcb_shard_blocking)
+if DO:
+    gt, _perm = parallel.degree_order(gt)
 plan = parallel.ShardPlan(parallel.shard_ranges(gt.row_offsets, P, vertex_cost=vc))
-shards = [parallel.DeviceShard(gt, *plan.owned(r), width) for r in range(P)]
+shards = [parallel.DeviceShard(gt, *plan.owned(r), width, 0, DO) for r in range(P)]
 dev = shards[0].device
 contrib = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(P)]
 ranks = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(P)]
@@ -47,7 +50,17 @@ for r, s in enumerate(shards):
     e1.record()
     torch.cuda.synchronize()
     times.append(e0.elapsed_time(e1) / 10)
+# per-kernel split of one step of each shard (library CUDA-event scopes)
+ctx = shards[0].ctx
+prof = []
+for r, s in enumerate(shards):
+    ctx.set_profiling(True)
+    s.step(contrib[r], ranks[r], 0.85, False)
+    prof.append({k: round(v[0], 4) for k, v in ctx.read_profile().items()})
+    ctx.set_profiling(False)
 out = {"graph": f"rmat:{scale}:16:1", "P": P, "width": width, "vertex_cost": vc,
+       "degree_ordered": DO,
+       "kernel_ms_per_shard_step": prof,
        "vertices_per_shard": [int(x) for x in np.diff(plan.ranges)],
        "edges_per_shard": [int(x) for x in np.diff(gt.row_offsets[plan.ranges])],
        "step_ms_per_shard": [round(t, 4) for t in times],
