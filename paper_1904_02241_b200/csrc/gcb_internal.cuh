@@ -197,6 +197,9 @@ struct gcb_blocked {
   gcb::DArray<uint32_t> hot_ids;     // [B][hot_k] source id of each slot (or ~0u)
   gcb::DArray<double> hotval;        // [B][hot_k] staged values for the next gather
   gcb::DArray<uint32_t> rstart;      // bit q: arena edge q starts a local row
+  gcb::DArray<uint32_t> hub_pack;    // hybrid hub blockings: per edge (row - tile_row) << 15 | slot
+                                     // (pr.cu ensure_hub_pack); ~0u past the arena
+  int hub_pack_state = 0;            // 0 not built, 1 built, -1 not packable (k_push_hot instead)
 
   // ---- workspaces (grown on demand) ----
   gcb::DArray<double> partials;  // [L]
@@ -214,6 +217,9 @@ struct gcb_blocked {
   gcb_blocked *hybrid = nullptr;     // degree-ordered copies: push blocking of the edges
                                      // from cold sources into hot destinations (owned)
   gcb::DArray<uint32_t> rl_perm;     // [n] original id -> renumbered id
+  int64_t n_live = -1;               // degree-ordered copies: ids [0, n_live) have out-degree
+                                     // > 0 (the rest contribute 0 forever); -1 = not counted
+  int64_t n_conn = 0;                // ... and [n_conn, n) are isolated (no edge either way)
   gcb_blocked *pending_hybrid = nullptr;  // build scratch of ensure_relabeled (owned)
   gcb_blocked *exact_pull = nullptr;      // push graphs: single-block pull blocking of the
                                           // transpose for the exact push (relabel.cu, owned)

@@ -413,6 +413,8 @@ void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
   // the pool may hand back the same addresses: never replay it afterwards
   destroy_pr_graph(bg->pr_graph);
   bg->pr_graph = nullptr;
+  bg->hub_pack.release();  // packed against the tile table rebuilt below
+  bg->hub_pack_state = 0;
   int64_t n = bg->n, B = bg->B;
   if (bg->cb) {
     // the CB kernels walk rows directly: out-degrees only

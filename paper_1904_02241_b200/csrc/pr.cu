@@ -400,9 +400,14 @@ __global__ void __launch_bounds__(512)
   __syncthreads();
   for (int64_t b = 0; b < B; ++b) {
     const int64_t s = bounds[b * (R + 1) + j], e = bounds[b * (R + 1) + j + 1];
-    for (int64_t p = s + threadIdx.x; p < e; p += blockDim.x) {
-      const int idx = (int)(id_map[p] - lo);
-      buf[idx] = __dadd_rn(buf[idx], partial[p]);
+    // a CTA-uniform trip count: every warp reaches the barrier converged
+    // (synccheck flagged the data-dependent exits of a p < e loop here)
+    for (int64_t q = s; q < e; q += blockDim.x) {
+      const int64_t p = q + threadIdx.x;
+      if (p < e) {
+        const int idx = (int)(id_map[p] - lo);
+        buf[idx] = __dadd_rn(buf[idx], partial[p]);
+      }
     }
     __syncthreads();
   }
@@ -434,19 +439,49 @@ __global__ void k_contributions(int64_t n, const double *__restrict__ ranks,
     out[v] = deg[v] > 0 ? __ddiv_rn(ranks[v], (double)deg[v]) : 0.0;
 }
 
-// ranks = r0; contributions = r0 / deg (VertexValueSet.initial kernels.py:80-89)
+// ranks = r0; contributions = r0 / deg (VertexValueSet.initial kernels.py:80-89);
+// sums = 0.  One 4-vertex quad per thread with 256-bit stores, like the
+// update.  ranks == nullptr (tol == 0): the ranks are first read after the
+// last iteration writes them, so they are not initialised.
 __global__ void k_pr_init(int64_t n, double r0, const uint32_t *__restrict__ deg,
                           double *__restrict__ ranks, double *__restrict__ contrib,
                           float *__restrict__ contrib32, double *__restrict__ sums) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    ranks[v] = r0;
+  const int64_t n4 = n >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint4 *D = reinterpret_cast<const uint4 *>(deg);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const uint4 d = __ldcs(D + i);
+    const uint32_t dg[4] = {d.x, d.y, d.z, d.w};
+    double c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = dg[k] ? __ddiv_rn(r0, (double)dg[k]) : 0.0;
+    if (ranks) st_f64x4(ranks + 4 * i, r0, r0, r0, r0);
+    if (contrib) st_f64x4(contrib + 4 * i, c[0], c[1], c[2], c[3]);
+    if (contrib32)
+      reinterpret_cast<float4 *>(contrib32)[i] =
+          make_float4(__double2float_rn(c[0]), __double2float_rn(c[1]), __double2float_rn(c[2]),
+                      __double2float_rn(c[3]));
+    st_f64x4(sums + 4 * i, 0.0, 0.0, 0.0, 0.0);
+  }
+  for (int64_t v = (n4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    if (ranks) ranks[v] = r0;
     const uint32_t dg = deg[v];
     const double c = dg ? __ddiv_rn(r0, (double)dg) : 0.0;
     if (contrib) contrib[v] = c;
     if (contrib32) contrib32[v] = __double2float_rn(c);
     sums[v] = 0.0;
   }
+}
+
+__global__ void k_count_nonzero_u32(int64_t n, const uint32_t *__restrict__ x,
+                                    unsigned long long *__restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += x[i] != 0u;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
 // rank update (kernels.py:398-399) fused with the L1 delta (399), the next
@@ -479,8 +514,10 @@ __global__ void __launch_bounds__(512, 2)
           make_float4(__double2float_rn(c[0]), __double2float_rn(c[1]), __double2float_rn(c[2]),
                       __double2float_rn(c[3]));
   };
+  // deltas == nullptr (tol == 0): the delta is dead, the old ranks are not read
+  const bool want_delta = RANKS && deltas;
   auto old = [&](int64_t i, double *o) {
-    if (RANKS) ld_rw_f64x4(ranks + 4 * i, o);
+    if (want_delta) ld_rw_f64x4(ranks + 4 * i, o);
     else o[0] = o[1] = o[2] = o[3] = 0.0;
   };
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -506,14 +543,14 @@ __global__ void __launch_bounds__(512, 2)
   }
   for (int64_t v = (n4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
     const double nr = __dadd_rn(base, __dmul_rn(damping, sums[v]));
-    if (RANKS) dsum += fabs(nr - ranks[v]);
+    if (want_delta) dsum += fabs(nr - ranks[v]);
     const double c = deg[v] ? div_deg<EXACT>(nr, deg[v]) : 0.0;
     if (RANKS) ranks[v] = nr;
     sums[v] = 0.0;
     if (contrib) contrib[v] = c;
     if (contrib32) contrib32[v] = __double2float_rn(c);
   }
-  if (!RANKS) return;
+  if (!want_delta) return;
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, d);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dsum;
@@ -703,86 +740,123 @@ __global__ void __launch_bounds__(1024, 1)
 
 // The hybrid hub pass (relabel.cu hybrid_split): every edge runs from a cold
 // source into a hub destination, and a cold source has few such edges, so a
-// 256-edge tile spans ~40 source rows on average (rmat:24).  k_push_hot loads
-// the values of a tile's first 32 rows when the tile starts (id_map -> vals,
-// two dependent L2 round trips exposed per tile) and every edge of a later
-// row loads id_map -> vals itself.  Here the row values of the NEXT tile are
-// fetched while this tile's adds run: the tile_row of tile t+2, the id_map
-// words of tile t+1 and then their values are issued one pipeline stage
-// ahead, two rows per lane (the first 64 rows of a tile) held in registers
-// and handed to the edges by shuffle; rows past 64 load directly.  The hub
-// adds use the two-word fixed point of fix_add.
+// 256-edge tile spans many source rows (rmat:22: median 5, 10% of tiles over
+// 64).  Its execution layout is packed once per graph (ensure_hub_pack): each
+// arena edge holds (its row - the tile's first row) << 15 | its hub slot, so
+// the kernel needs no row-start bitmap, no tile scan and no recode test --
+// an edge is one LDS.64 of its row's value and the two 32-bit shared atomics
+// of fix_add.  A tile's row values are fetched two pipeline stages ahead
+// (tile_row three tiles ahead, the id_map words of tile t+2, the values of
+// tile t+1, two rows per lane), converted to the table's fixed point once per
+// row and parked in the warp's slice of shared memory; rows 64..127 of a long
+// tile are loaded when it starts, and edges of rows past 128 take a second,
+// warp-uniform loop.  The bitmap form of this pass spent 432 warp
+// instructions per tile and stalled on its id_map -> value chain (ncu,
+// profiles/r2_hub_ncu.txt).
+constexpr int kHubRows = 128;         // row values per warp parked in shared memory
+constexpr uint32_t kPackNone = ~0u;   // hub_pack entry past the arena
+constexpr int kPackSlotBits = 15;     // slots < 2^15 - 32 (the 32 lane dummies follow)
+
+// fix_add on shared-memory addresses (a_lo / a_hi: the slot's two words).
+// Unpredicated: an edge that must not add is aimed at its lane's dummy slot
+// with 0 (no branch around the atomics, and no two lanes share a dummy).
+__device__ __forceinline__ void fix_add_s(uint32_t a_lo, uint32_t a_hi, unsigned long long add) {
+  const unsigned alo = (unsigned)add, ahi = (unsigned)(add >> 32);
+  unsigned old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a_lo), "r"(alo));
+  const unsigned carry = (old + alo < old) ? 1u : 0u;
+  asm volatile("red.shared.add.u32 [%0], %1;" : : "r"(a_hi), "r"(ahi + carry));
+}
+
+__device__ __forceinline__ unsigned long long to_fix(double x) {
+  return __double2ull_rn(x * kFixScale);
+}
+
 // the tile loop of k_push_hub (one warp, tiles t, t + stride, ...)
-__device__ __forceinline__ void hub_tiles(
-    const uint32_t *__restrict__ xcol, const uint32_t *__restrict__ rstart,
-    const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0, int64_t ntiles,
-    uint32_t Lb, const uint32_t *__restrict__ id_map_b, const double *__restrict__ vals,
-    double *__restrict__ sums, unsigned *s_lo, unsigned *s_hi, int64_t t, int64_t stride,
-    int lane, uint64_t pol_stream) {
+__device__ __forceinline__ void hub_tiles(const uint32_t *__restrict__ pack,
+                                          const uint32_t *__restrict__ tile_row, uint32_t ntiles,
+                                          uint32_t Lb, const uint32_t *__restrict__ id_map_b,
+                                          const double *__restrict__ vals, uint32_t s_lo_addr,
+                                          uint32_t s_hi_addr, unsigned long long *s_rows,
+                                          uint32_t dummy, uint32_t t, uint32_t stride, int lane,
+                                          uint64_t pol_stream) {
   constexpr int V = kTileV, T = kTileT;
-  constexpr uint32_t kHot = 0x80000000u;
+  constexpr uint32_t kSlotMask = (1u << kPackSlotBits) - 1u;
   const unsigned FULL = 0xffffffffu;
   auto row_id = [&](uint32_t r) { return r < Lb ? __ldg(id_map_b + r) : 0u; };
-  // pipeline state: tile t's words and row values, tile t+1's first row
-  uint32_t c[V], fw, r0, r0n = 0;
-  double rvA, rvB;
-  {
-    const int64_t abase = (t0 + t) * T;
-    ld_stream_u32x8(xcol + abase + lane * V, pol_stream, c);
-    fw = rstart[(abase >> 5) + (lane < 8 ? lane : 8)];
-    r0 = tile_row[t];
-    if (t + stride < ntiles) r0n = tile_row[t + stride];
-    rvA = __ldg(vals + row_id(r0 + lane));
-    rvB = __ldg(vals + row_id(r0 + 32 + lane));
+  auto words = [&](uint32_t tt, uint32_t (&w)[V]) {
+    ld_stream_u32x8(pack + (size_t)tt * T + lane * V, pol_stream, w);
+  };
+  // pipeline: tile t's words and row values, tile t+1's row ids, the first
+  // rows of tiles t+1 and t+2
+  uint32_t c[V];
+  words(t, c);
+  uint32_t r0 = tile_row[t], r0n = 0, r0nn = 0, idA = 0, idB = 0;
+  if (t + stride < ntiles) {
+    r0n = tile_row[t + stride];
+    idA = row_id(r0n + lane);
+    idB = row_id(r0n + 32 + lane);
+    if (t + 2 * stride < ntiles) r0nn = tile_row[t + 2 * stride];
   }
+  double rvA = __ldg(vals + row_id(r0 + lane)), rvB = __ldg(vals + row_id(r0 + 32 + lane));
   for (; t < ntiles; t += stride) {
-    const int64_t abase = (t0 + t) * T;
-    const int64_t tn = t + stride;
-    const bool has_next = tn < ntiles;
-    // stage 1 for tile t+1: its arena words and its rows' ids; tile t+2's first row
-    uint32_t cn[V] = {0, 0, 0, 0, 0, 0, 0, 0}, fwn = 0, r0nn = 0, idA = 0, idB = 0;
-    if (has_next) {
-      const int64_t nb = (t0 + tn) * T;
-      ld_stream_u32x8(xcol + nb + lane * V, pol_stream, cn);
-      fwn = rstart[(nb >> 5) + (lane < 8 ? lane : 8)];
-      if (tn + stride < ntiles) r0nn = tile_row[tn + stride];
-      idA = row_id(r0n + lane);
-      idB = row_id(r0n + 32 + lane);
-    }
-    // this tile's rows
-    const int llo = es > abase ? (int)(es - abase) : 0;
-    const int lhi = ee - abase < T ? (int)(ee - abase) : T;
-    const TileBits tb = tile_bits(fw, llo, lhi, lane);
-    const int cnt = __popc(tb.bits);
-    int incl = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, d);
-      if (lane >= d) incl += y;
-    }
-    // stage 2 for tile t+1: the row values (the ids have had the scan's time)
+    const uint32_t tn = t + stride, tnn = tn + stride;
+    uint32_t cn[V], idAn = 0, idBn = 0, r0nnn = 0;
     double rvAn = 0.0, rvBn = 0.0;
-    if (has_next) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) cn[k] = kPackNone;
+    if (tn < ntiles) {  // tile t+1: words and values (its ids landed an iteration ago)
+      words(tn, cn);
       rvAn = __ldg(vals + idA);
       rvBn = __ldg(vals + idB);
     }
-    const int kf = tb.vm ? __ffs(tb.vm) - 1 : 0;
-    uint32_t rr = (uint32_t)(incl - cnt) + ((tb.bits >> kf) & 1u);
+    if (tnn < ntiles) {  // tile t+2: row ids; tile t+3: first row
+      idAn = row_id(r0nn + lane);
+      idBn = row_id(r0nn + 32 + lane);
+      if (tnn + stride < ntiles) r0nnn = tile_row[tnn + stride];
+    }
+    // this tile's row values, fixed point, in the warp's slice.  Row indices
+    // grow along the tile, so lane 31's last entry bounds them (a padding
+    // entry past the arena reads as "long" and costs one extra load).
+    __syncwarp();  // the previous tile's readers are done with the slice
+    s_rows[lane] = to_fix(rvA);
+    s_rows[32 + lane] = to_fix(rvB);
+    const uint32_t rr_max = __shfl_sync(FULL, c[V - 1], 31) >> kPackSlotBits;
+    if (rr_max >= 64) {
+      const double xc = __ldg(vals + row_id(r0 + 64 + lane));
+      const double xd = rr_max >= 96 ? __ldg(vals + row_id(r0 + 96 + lane)) : 0.0;
+      s_rows[64 + lane] = to_fix(xc);
+      s_rows[96 + lane] = to_fix(xd);
+    }
+    __syncwarp();
+    uint32_t omask = 0;  // edges of rows past kHubRows
 #pragma unroll
     for (int k = 0; k < V; ++k) {
-      if (k > kf && ((tb.bits >> k) & 1u)) ++rr;
-      const double xa = __shfl_sync(FULL, rvA, rr & 31);
-      const double xb = __shfl_sync(FULL, rvB, rr & 31);
-      if (!((tb.vm >> k) & 1u)) continue;
-      const double x = rr < 32 ? xa : (rr < 64 ? xb : __ldg(vals + __ldg(id_map_b + r0 + rr)));
-      if (c[k] & kHot) fix_add(s_lo, s_hi, c[k] & ~kHot, __double2ull_rn(x * kFixScale));
-      else atomicAdd(sums + c[k], x);  // not a hub (cannot happen for hybrid_split edges)
+      const uint32_t e = c[k];
+      const uint32_t rr = e >> kPackSlotBits;
+      const bool add = rr < (uint32_t)kHubRows;  // kPackNone: rr = 2^17 - 1
+      if (!add && e != kPackNone) omask |= 1u << k;
+      const unsigned long long f = add ? s_rows[rr] : 0ull;
+      const uint32_t slot = (add ? (e & kSlotMask) : dummy) * 4u;
+      fix_add_s(s_lo_addr + slot, s_hi_addr + slot, f);
+    }
+    if (__any_sync(FULL, omask != 0u)) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if (!((omask >> k) & 1u)) continue;
+        const uint32_t e = c[k];
+        const double x = __ldg(vals + __ldg(id_map_b + r0 + (e >> kPackSlotBits)));
+        const uint32_t slot = (e & kSlotMask) * 4u;
+        fix_add_s(s_lo_addr + slot, s_hi_addr + slot, to_fix(x));
+      }
     }
 #pragma unroll
     for (int k = 0; k < V; ++k) c[k] = cn[k];
-    fw = fwn;
     r0 = r0n;
     r0n = r0nn;
+    r0nn = r0nnn;
+    idA = idAn;
+    idB = idBn;
     rvA = rvAn;
     rvB = rvBn;
   }
@@ -790,29 +864,92 @@ __device__ __forceinline__ void hub_tiles(
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
-    k_push_hub(const uint32_t *__restrict__ xcol, const uint32_t *__restrict__ rstart,
-               const uint32_t *__restrict__ tile_row, int64_t es, int64_t ee, int64_t t0,
-               int64_t ntiles, uint32_t Lb, const uint32_t *__restrict__ id_map_b,
+    k_push_hub(const uint32_t *__restrict__ pack, const uint32_t *__restrict__ tile_row,
+               uint32_t ntiles, uint32_t Lb, const uint32_t *__restrict__ id_map_b,
                const uint32_t *__restrict__ hot_ids_b, int hot, const double *__restrict__ vals,
                double *__restrict__ sums) {
-  constexpr int V = kTileV, T = kTileT;
-  constexpr uint32_t kHot = 0x80000000u;
   extern __shared__ double smem_d[];
-  unsigned *s_lo = reinterpret_cast<unsigned *>(smem_d), *s_hi = s_lo + hot;
-  const unsigned FULL = 0xffffffffu;
+  // hub table: hot slots + one dummy slot per lane, low words then high words
+  const int slots = hot + 32;
+  unsigned *s_lo = reinterpret_cast<unsigned *>(smem_d), *s_hi = s_lo + slots;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // per-warp row-value slices after the table
+  unsigned long long *s_rows = reinterpret_cast<unsigned long long *>(smem_d + slots) + wid * kHubRows;
   const uint64_t pol_stream = policy_evict_first();
-  for (int i = threadIdx.x; i < hot; i += blockDim.x) smem_d[i] = 0.0;
+  for (int i = threadIdx.x; i < slots; i += blockDim.x) smem_d[i] = 0.0;
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * NW;
-  int64_t t = (int64_t)blockIdx.x * NW + wid;
-  if (t < ntiles) hub_tiles(xcol, rstart, tile_row, es, ee, t0, ntiles, Lb, id_map_b, vals,
-                            sums, s_lo, s_hi, t, stride, lane, pol_stream);
+  const uint32_t t = blockIdx.x * NW + wid;
+  if (t < ntiles)
+    hub_tiles(pack, tile_row, ntiles, Lb, id_map_b, vals, (uint32_t)__cvta_generic_to_shared(s_lo),
+              (uint32_t)__cvta_generic_to_shared(s_hi), s_rows, (uint32_t)(hot + lane), t,
+              gridDim.x * NW, lane, pol_stream);
   __syncthreads();
-  for (int i = threadIdx.x; i < hot; i += blockDim.x) {
-    const double v = (double)(((unsigned long long)s_hi[i] << 32) | s_lo[i]) * kFixInv;
-    if (v != 0.0) atomicAdd(sums + hot_ids_b[i], v);
+  // flush: four slots per thread in flight (the hub ids are global loads)
+  for (int i0 = threadIdx.x; i0 < hot; i0 += 4 * blockDim.x) {
+    uint32_t id[4];
+    double v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j * blockDim.x;
+      id[j] = i < hot ? __ldg(hot_ids_b + i) : 0u;
+      v[j] = i < hot ? (double)(((unsigned long long)s_hi[i] << 32) | s_lo[i]) * kFixInv : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (v[j] != 0.0) atomicAdd(sums + id[j], v[j]);
   }
+}
+
+// hub_pack[q] = (row(q) - tile_row[tile(q)]) << 15 | slot(q) for the arena edges of a
+// single-block hub blocking; *bad counts edges the format cannot hold
+__global__ void k_hub_pack(int64_t Lb, const uint32_t *__restrict__ lro_b,
+                           const uint32_t *__restrict__ tile_row_b, const uint32_t *__restrict__ xcol,
+                           uint32_t slot_cap, uint32_t *__restrict__ pack,
+                           unsigned long long *__restrict__ bad) {
+  constexpr uint32_t kHot = 0x80000000u;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long nb = 0;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Lb; r += nw) {
+    const uint32_t s = lro_b[r], e = lro_b[r + 1];
+    for (uint32_t q = s + lane; q < e; q += 32) {
+      const uint32_t rr = (uint32_t)r - tile_row_b[q / kTileT];
+      const uint32_t x = xcol[q], slot = x & ~kHot;
+      const bool ok = (x & kHot) && rr < 256u && slot < slot_cap;
+      pack[q] = ok ? (rr << kPackSlotBits) | slot : 0u;
+      nb += !ok;
+    }
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
+// Builds the packed hub layout once per blocking: single-block push blockings
+// whose every edge is a recoded hub (relabel.cu hybrid_split guarantees it:
+// the blocking holds only hub destinations); anything else keeps k_push_hot.
+static bool ensure_hub_pack(gcb_ctx *ctx, gcb_blocked *bg) {
+  if (bg->hub_pack_state) return bg->hub_pack_state > 0;
+  bg->hub_pack_state = -1;
+  const int64_t cap = (int64_t(1) << kPackSlotBits) - 32;
+  if (bg->B != 1 || bg->hot_k <= 0 || bg->hot_k > cap || bg->m == 0 || !bg->xcol.p ||
+      bg->h_edge_starts[0] != 0 || bg->h_tile_t0[0] != 0)
+    return false;
+  bg->hub_pack.alloc(bg->m + kColPad);
+  GCB_CUDA(cudaMemsetAsync(bg->hub_pack.p + bg->m, 0xff, kColPad * sizeof(uint32_t), ctx->stream));
+  DArray<unsigned long long> bad(1);
+  GCB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), ctx->stream));
+  const int64_t Lb = bg->h_row_starts[1] - bg->h_row_starts[0];
+  k_hub_pack<<<grid_for(Lb * 32, 256, 65536), 256, 0, ctx->stream>>>(
+      Lb, bg->lro.p, bg->tile_row.p, bg->xcol.p, (uint32_t)bg->hot_k, bg->hub_pack.p, bad.p);
+  after_launch(ctx, "k_hub_pack");
+  unsigned long long h = 0;
+  d2h(ctx, &h, bad.p, 1);
+  sync(ctx);
+  if (h) {
+    bg->hub_pack.release();
+    return false;
+  }
+  bg->hub_pack_state = 1;
+  return true;
 }
 
 __global__ void k_add_range(int64_t lo, int64_t hi, const double *__restrict__ local,
@@ -1053,14 +1190,15 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
       ensure_smem_attrs(ctx, (const void *)k_push_hot<false, true>, smem);
       const unsigned gh = grid_for(nt * 32, 1024, (int64_t)ctx->num_sms);
       constexpr int kHubNW = 32;
-      const size_t smem_hub = smem;
+      const size_t smem_hub = (size_t)(hot + 32) * sizeof(double) +
+                              (size_t)kHubNW * kHubRows * sizeof(unsigned long long);
       const char *hv = getenv("GCB_HUB_KERNEL");
       if (nonneg && !wgt && !getenv("GCB_NO_FIX") && !(hv && hv[0] == '0') &&
-          smem_hub <= (size_t)max_smem_optin(ctx)) {
+          smem_hub <= (size_t)max_smem_optin(ctx) && ensure_hub_pack(ctx, bg)) {
         ensure_smem_attrs(ctx, (const void *)k_push_hub<kHubNW>, smem_hub);
         k_push_hub<kHubNW><<<gh, kHubNW * 32, smem_hub, ctx->stream>>>(
-            bg->xcol.p, bg->rstart.p, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt,
-            (uint32_t)Lb, bg->id_map.p + rs, bg->hot_ids.p + b * bg->hot_k, hot, vals, sums);
+            bg->hub_pack.p, bg->tile_row.p, (uint32_t)nt, (uint32_t)Lb, bg->id_map.p,
+            bg->hot_ids.p, hot, vals, sums);
         after_launch(ctx, "k_push_hub");
         continue;
       }
@@ -1254,9 +1392,34 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   float *contrib32 = f32 ? bg->contrib32.p : nullptr;
   {
     ProfScope ps(ctx, 3);
-    k_pr_init<<<upd_grid, 256, 0, ctx->stream>>>(n, r0, deg, ranks_dev, bg->contrib.p, contrib32,
+    k_pr_init<<<upd_grid, 256, 0, ctx->stream>>>(n, r0, deg, tol > 0.0 ? ranks_dev : nullptr,
+                                                 contrib ? contrib : bg->contrib.p, contrib32,
                                                  bg->sums.p);
     after_launch(ctx, "k_pr_init");
+  }
+  // Live range of the degree-ordered copy.  Its ids are sorted by descending
+  // out-degree, so [n_live, n) is every vertex with out-degree 0: its
+  // contribution is 0 in every iteration (kernels.py:185-191), and with
+  // tol == 0 its intermediate ranks are never read (no delta; only the last
+  // iteration's ranks are returned).  Those iterations update [0, n_live)
+  // only (rmat:24: 7.38M of 16.8M vertices -- most R-MAT vertices are
+  // isolated); the last one updates every vertex, after clearing the sums of
+  // [n_live, n), which the skipped updates did not clear.  The ranks are
+  // unchanged: the skipped work is dead.
+  int64_t n_upd = n;
+  if (bg->is_relabeled && tol == 0.0 && !exact && !push && !f32 && !deg_override) {
+    if (bg->n_live < 0) {
+      DArray<unsigned long long> cnt(1);
+      GCB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
+      k_count_nonzero_u32<<<grid_for(n, 256, 4096), 256, 0, ctx->stream>>>(n, deg, cnt.p);
+      after_launch(ctx, "k_count_nonzero_u32");
+      unsigned long long h = 0;
+      d2h(ctx, &h, cnt.p, 1);
+      sync(ctx);
+      bg->n_live = (int64_t)h;
+    }
+    const char *lv = getenv("GCB_FULL_UPDATE");  // A/B knob: 1 updates every vertex
+    if (!(lv && lv[0] == '1')) n_upd = bg->n_live;
   }
   // one iteration's launches (no host synchronisation: also the graph body);
   // with_ranks = false only where the ranks and delta are dead (tol == 0, not
@@ -1280,9 +1443,9 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
     }
     {
       ProfScope ps(ctx, 2);
-      launch_update(ctx, exact, n, base, damping, bg->sums.p, ranks_dev, deg,
-                    contrib ? contrib : (push ? bg->contrib.p : nullptr), contrib32, bg->deltas.p,
-                    with_ranks);
+      launch_update(ctx, exact, with_ranks ? n : n_upd, base, damping, bg->sums.p, ranks_dev, deg,
+                    contrib ? contrib : (push ? bg->contrib.p : nullptr), contrib32,
+                    tol > 0.0 ? bg->deltas.p : nullptr, with_ranks);
     }
     if (tol > 0.0) {
       k_reduce_sum<<<1, 1024, 0, ctx->stream>>>(bg->deltas.p, update_grid(ctx, n), delta_dev);
@@ -1294,7 +1457,10 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   const char *kr = getenv("GCB_KEEP_RANKS");  // 1: full update every iteration (A/B knob)
   const bool keep_ranks = kr && kr[0] == '1';
   for (int k = 0; k < max_iters; ++k) {
-    iterate(tol > 0.0 || k == max_iters - 1 || keep_ranks);
+    const bool last = tol > 0.0 || k == max_iters - 1 || keep_ranks;
+    if (last && k > 0 && n_upd < n)
+      GCB_CUDA(cudaMemsetAsync(bg->sums.p + n_upd, 0, (n - n_upd) * sizeof(double), ctx->stream));
+    iterate(last);
     ++it;
     if (tol > 0.0) {
       d2h(ctx, hdelta, delta_dev, 1);
@@ -1573,7 +1739,7 @@ int gcb_pr_shard_init(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, con
                       double *contrib_dev, double *ranks_dev) {
   GCB_API_BEGIN
   GCB_REQUIRE(ctx && bg && deg_dev && contrib_dev && ranks_dev, "NULL argument");
-  GCB_REQUIRE(0 <= v0 && v0 <= v1 && v1 <= bg->n && bg->n > 0, "bad shard range");
+  GCB_REQUIRE(0 <= v0 && v0 <= v1 && v1 <= bg->n && bg->n > 0 && (v0 % 4) == 0, "bad shard range");
   GCB_REQUIRE(bg->direction == 0, "sharded PageRank runs on a pull blocking");
   DeviceGuard dg(ctx->device);
   ensure_derived(ctx, bg);
