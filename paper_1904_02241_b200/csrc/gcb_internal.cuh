@@ -200,6 +200,8 @@ struct gcb_blocked {
   gcb::DArray<uint32_t> hub_pack;    // hybrid hub blockings: per edge (row - tile_row) << 15 | slot
                                      // (pr.cu ensure_hub_pack); ~0u past the arena
   int hub_pack_state = 0;            // 0 not built, 1 built, -1 not packable (k_push_hot instead)
+  gcb::DArray<unsigned long long> hub_acc;  // [hot_k] k_push_hub's cross-CTA fixed-point sums
+                                            // (zero between passes: k_hub_fold clears them)
 
   // ---- workspaces (grown on demand) ----
   gcb::DArray<double> partials;  // [L]

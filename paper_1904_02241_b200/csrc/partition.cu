@@ -414,6 +414,7 @@ void ensure_derived(gcb_ctx *ctx, gcb_blocked *bg) {
   destroy_pr_graph(bg->pr_graph);
   bg->pr_graph = nullptr;
   bg->hub_pack.release();  // packed against the tile table rebuilt below
+  bg->hub_acc.release();
   bg->hub_pack_state = 0;
   int64_t n = bg->n, B = bg->B;
   if (bg->cb) {

@@ -396,7 +396,10 @@ __global__ void __launch_bounds__(512)
   const int64_t lo = j * kMergeK;
   const int64_t hi = (lo + kMergeK < n) ? lo + kMergeK : n;
   const int width = (int)(hi - lo);
-  for (int i = threadIdx.x; i < width; i += blockDim.x) buf[i] = 0.0;
+  for (int i0 = 0; i0 < kMergeK; i0 += blockDim.x) {  // CTA-uniform trip count
+    const int i = i0 + threadIdx.x;
+    if (i < kMergeK) buf[i] = 0.0;
+  }
   __syncthreads();
   for (int64_t b = 0; b < B; ++b) {
     const int64_t s = bounds[b * (R + 1) + j], e = bounds[b * (R + 1) + j + 1];
@@ -768,6 +771,19 @@ __device__ __forceinline__ void fix_add_s(uint32_t a_lo, uint32_t a_hi, unsigned
   asm volatile("red.shared.add.u32 [%0], %1;" : : "r"(a_hi), "r"(ahi + carry));
 }
 
+// two fix_add_s with both low-word atomics issued first
+__device__ __forceinline__ void fix_add2_s(uint32_t a_lo, uint32_t a_hi, unsigned long long add_a,
+                                           uint32_t b_lo, uint32_t b_hi, unsigned long long add_b) {
+  const unsigned alo = (unsigned)add_a, ahi = (unsigned)(add_a >> 32);
+  const unsigned blo = (unsigned)add_b, bhi = (unsigned)(add_b >> 32);
+  unsigned olda, oldb;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(olda) : "r"(a_lo), "r"(alo));
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(oldb) : "r"(b_lo), "r"(blo));
+  const unsigned ca = (olda + alo < olda) ? 1u : 0u, cb = (oldb + blo < oldb) ? 1u : 0u;
+  asm volatile("red.shared.add.u32 [%0], %1;" : : "r"(a_hi), "r"(ahi + ca));
+  asm volatile("red.shared.add.u32 [%0], %1;" : : "r"(b_hi), "r"(bhi + cb));
+}
+
 __device__ __forceinline__ unsigned long long to_fix(double x) {
   return __double2ull_rn(x * kFixScale);
 }
@@ -830,15 +846,23 @@ __device__ __forceinline__ void hub_tiles(const uint32_t *__restrict__ pack,
     }
     __syncwarp();
     uint32_t omask = 0;  // edges of rows past kHubRows
+    // two edges per step: both low-word atomics are in flight before either
+    // carry is needed
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const uint32_t e = c[k];
-      const uint32_t rr = e >> kPackSlotBits;
-      const bool add = rr < (uint32_t)kHubRows;  // kPackNone: rr = 2^17 - 1
-      if (!add && e != kPackNone) omask |= 1u << k;
-      const unsigned long long f = add ? s_rows[rr] : 0ull;
-      const uint32_t slot = (add ? (e & kSlotMask) : dummy) * 4u;
-      fix_add_s(s_lo_addr + slot, s_hi_addr + slot, f);
+    for (int k = 0; k < V; k += 2) {
+      unsigned long long f[2];
+      uint32_t slot[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t e = c[k + j];
+        const uint32_t rr = e >> kPackSlotBits;
+        const bool add = rr < (uint32_t)kHubRows;  // kPackNone: rr = 2^17 - 1
+        if (!add && e != kPackNone) omask |= 1u << (k + j);
+        f[j] = add ? s_rows[rr] : 0ull;
+        slot[j] = (add ? (e & kSlotMask) : dummy) * 4u;
+      }
+      fix_add2_s(s_lo_addr + slot[0], s_hi_addr + slot[0], f[0], s_lo_addr + slot[1],
+                 s_hi_addr + slot[1], f[1]);
     }
     if (__any_sync(FULL, omask != 0u)) {
 #pragma unroll
@@ -862,12 +886,14 @@ __device__ __forceinline__ void hub_tiles(const uint32_t *__restrict__ pack,
   }
 }
 
+// Each CTA adds its table into hub_acc (u64 fixed point: coalesced 64-bit
+// integer REDs, no id lookup on the flush path, and the cross-CTA sum is
+// order-independent); k_hub_fold then adds hub_acc into sums once.
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
     k_push_hub(const uint32_t *__restrict__ pack, const uint32_t *__restrict__ tile_row,
-               uint32_t ntiles, uint32_t Lb, const uint32_t *__restrict__ id_map_b,
-               const uint32_t *__restrict__ hot_ids_b, int hot, const double *__restrict__ vals,
-               double *__restrict__ sums) {
+               uint32_t ntiles, uint32_t Lb, const uint32_t *__restrict__ id_map_b, int hot,
+               const double *__restrict__ vals, unsigned long long *__restrict__ hub_acc) {
   extern __shared__ double smem_d[];
   // hub table: hot slots + one dummy slot per lane, low words then high words
   const int slots = hot + 32;
@@ -884,19 +910,22 @@ __global__ void __launch_bounds__(NW * 32, 1)
               (uint32_t)__cvta_generic_to_shared(s_hi), s_rows, (uint32_t)(hot + lane), t,
               gridDim.x * NW, lane, pol_stream);
   __syncthreads();
-  // flush: four slots per thread in flight (the hub ids are global loads)
-  for (int i0 = threadIdx.x; i0 < hot; i0 += 4 * blockDim.x) {
-    uint32_t id[4];
-    double v[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = i0 + j * blockDim.x;
-      id[j] = i < hot ? __ldg(hot_ids_b + i) : 0u;
-      v[j] = i < hot ? (double)(((unsigned long long)s_hi[i] << 32) | s_lo[i]) * kFixInv : 0.0;
+  for (int i = threadIdx.x; i < hot; i += blockDim.x) {
+    const unsigned long long v = ((unsigned long long)s_hi[i] << 32) | s_lo[i];
+    if (v) atomicAdd(hub_acc + i, v);
+  }
+}
+
+// sums[hub] += hub_acc[slot] (fixed point -> f64), and hub_acc back to zero
+__global__ void k_hub_fold(int hot, const uint32_t *__restrict__ hot_ids_b,
+                           unsigned long long *__restrict__ hub_acc, double *__restrict__ sums) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < hot; i += gridDim.x * blockDim.x) {
+    const unsigned long long v = hub_acc[i];
+    if (v) {
+      const uint32_t id = hot_ids_b[i];
+      sums[id] = __dadd_rn(sums[id], (double)v * kFixInv);
+      hub_acc[i] = 0ull;
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (v[j] != 0.0) atomicAdd(sums + id[j], v[j]);
   }
 }
 
@@ -1196,10 +1225,17 @@ void push_scatter(gcb_ctx *ctx, gcb_blocked *bg, const double *vals, double *sum
       if (nonneg && !wgt && !getenv("GCB_NO_FIX") && !(hv && hv[0] == '0') &&
           smem_hub <= (size_t)max_smem_optin(ctx) && ensure_hub_pack(ctx, bg)) {
         ensure_smem_attrs(ctx, (const void *)k_push_hub<kHubNW>, smem_hub);
+        if (!bg->hub_acc.p) {
+          bg->hub_acc.alloc(hot);
+          GCB_CUDA(cudaMemsetAsync(bg->hub_acc.p, 0, hot * sizeof(unsigned long long), ctx->stream));
+        }
         k_push_hub<kHubNW><<<gh, kHubNW * 32, smem_hub, ctx->stream>>>(
-            bg->hub_pack.p, bg->tile_row.p, (uint32_t)nt, (uint32_t)Lb, bg->id_map.p,
-            bg->hot_ids.p, hot, vals, sums);
+            bg->hub_pack.p, bg->tile_row.p, (uint32_t)nt, (uint32_t)Lb, bg->id_map.p, hot, vals,
+            bg->hub_acc.p);
         after_launch(ctx, "k_push_hub");
+        k_hub_fold<<<grid_for(hot, 256, 1024), 256, 0, ctx->stream>>>(hot, bg->hot_ids.p,
+                                                                      bg->hub_acc.p, sums);
+        after_launch(ctx, "k_hub_fold");
         continue;
       }
       if (nonneg && !wgt && !getenv("GCB_NO_FIX"))
