@@ -831,13 +831,15 @@ __device__ __forceinline__ void hub_tiles(const uint32_t *__restrict__ pack,
       idBn = row_id(r0nn + 32 + lane);
       if (tnn + stride < ntiles) r0nnn = tile_row[tnn + stride];
     }
-    // this tile's row values, fixed point, in the warp's slice.  Row indices
-    // grow along the tile, so lane 31's last entry bounds them (a padding
-    // entry past the arena reads as "long" and costs one extra load).
+    // this tile's row values, fixed point, in the warp's slice
     __syncwarp();  // the previous tile's readers are done with the slice
     s_rows[lane] = to_fix(rvA);
     s_rows[32 + lane] = to_fix(rvB);
-    const uint32_t rr_max = __shfl_sync(FULL, c[V - 1], 31) >> kPackSlotBits;
+    uint32_t lane_max = 0;  // entries are in bank order, not row order (ensure_hub_pack)
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (c[k] != kPackNone) lane_max = max(lane_max, c[k] >> kPackSlotBits);
+    const uint32_t rr_max = __reduce_max_sync(FULL, lane_max);
     if (rr_max >= 64) {
       const double xc = __ldg(vals + row_id(r0 + 64 + lane));
       const double xd = rr_max >= 96 ? __ldg(vals + row_id(r0 + 96 + lane)) : 0.0;
@@ -952,6 +954,48 @@ __global__ void k_hub_pack(int64_t Lb, const uint32_t *__restrict__ lro_b,
   if (nb) atomicAdd(bad, nb);
 }
 
+// Reorders every 256-entry tile of hub_pack by shared-memory bank of its slot
+// (slot mod 32).  Lane l runs entries 8l..8l+7 in steps k = 0..7, so step k
+// takes sorted positions k, 8+k, ..., and no two edges of one step share a bank
+// unless a bank holds more than 8 of the tile's edges: the atomics of a step
+// go out in one wavefront instead of ~3.7 (ncu, r2_hub_ncu.txt).  Integer
+// fixed-point adds commute and every entry carries its own row offset, so any
+// order within a tile gives the same table.  One warp per tile.
+__global__ void __launch_bounds__(256) k_hub_bank_sort(int64_t ntiles, uint32_t *__restrict__ pack) {
+  __shared__ uint32_t s_ent[8][kTileT];
+  __shared__ uint32_t s_cnt[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * 8 + w;
+  if (t >= ntiles) return;
+  uint32_t *tile = pack + t * kTileT;
+  s_cnt[w][lane] = 0;
+  __syncwarp();
+  uint32_t e[kTileV], b[kTileV];
+#pragma unroll
+  for (int k = 0; k < kTileV; ++k) {
+    e[k] = tile[lane * kTileV + k];
+    b[k] = (e[k] == kPackNone ? 31u : e[k]) & 31u;
+    atomicAdd(&s_cnt[w][b[k]], 1u);
+  }
+  __syncwarp();
+  // exclusive prefix of the 32 bank counts (lane = bank)
+  const uint32_t cnt = s_cnt[w][lane];
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  __syncwarp();
+  s_cnt[w][lane] = incl - cnt;  // cursor of each bank
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < kTileV; ++k) s_ent[w][atomicAdd(&s_cnt[w][b[k]], 1u)] = e[k];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < kTileV; ++k) tile[lane * kTileV + k] = s_ent[w][lane * kTileV + k];
+}
+
 // Builds the packed hub layout once per blocking: single-block push blockings
 // whose every edge is a recoded hub (relabel.cu hybrid_split guarantees it:
 // the blocking holds only hub destinations); anything else keeps k_push_hot.
@@ -970,6 +1014,12 @@ static bool ensure_hub_pack(gcb_ctx *ctx, gcb_blocked *bg) {
   k_hub_pack<<<grid_for(Lb * 32, 256, 65536), 256, 0, ctx->stream>>>(
       Lb, bg->lro.p, bg->tile_row.p, bg->xcol.p, (uint32_t)bg->hot_k, bg->hub_pack.p, bad.p);
   after_launch(ctx, "k_hub_pack");
+  const int64_t ntiles = bg->h_tile_base[1] - bg->h_tile_base[0];
+  const char *ns = getenv("GCB_HUB_NOSORT");  // A/B knob: keep the arena order
+  if (!(ns && ns[0] == '1')) {
+    k_hub_bank_sort<<<(unsigned)ceil_div(ntiles, 8), 256, 0, ctx->stream>>>(ntiles, bg->hub_pack.p);
+    after_launch(ctx, "k_hub_bank_sort");
+  }
   unsigned long long h = 0;
   d2h(ctx, &h, bad.p, 1);
   sync(ctx);
