@@ -1864,7 +1864,7 @@ int gcb_pr_shard_step(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, dou
     ProfScope ps(ctx, 2);
     launch_update(ctx, flags & GCB_FLAG_EXACT, cnt, (1.0 - damping) / (double)bg->n, damping,
                   bg->sums.p + v0, ranks_dev + v0, deg_dev + v0, contrib_dev + v0, nullptr,
-                  bg->deltas.p);
+                  delta_dev ? bg->deltas.p : nullptr);  // no delta wanted: old ranks unread
   }
   if (delta_dev) {
     if (cnt) {

@@ -156,12 +156,14 @@ static int64_t hybrid_hub_slots(gcb_ctx *ctx) {
   return want < cap ? want : cap;
 }
 
-// The push pass has a fixed cost -- its own launch, and every CTA flushes its
-// hub table (num_sms x slots global adds) -- against a per-edge saving over the
-// pull gather.  Fitted on rmat:21/22/24/25:44 (ms per iteration, hybrid minus
-// pull-only: +0.032, +0.024, -0.015, -0.26 for 9.7M/19M/64M/370M hub edges):
-// +40 us fixed, -0.85 ps per edge moved, break-even near 13 x num_sms x slots.
-constexpr int64_t kHybridMinEdgesPerSlot = 14;
+// The push pass has a fixed cost -- its own launch, every CTA zeroes and
+// flushes its hub table, the fold -- against a per-edge saving over the pull
+// gather.  With the packed hub kernel (pr.cu k_push_hub) the measured gather +
+// hub time per iteration, hybrid vs pull-only, is 0.0963 vs 0.0955 ms at
+// rmat:21 (9.7M hub edges) and 0.172 vs 0.190 ms at rmat:22 (19M): break-even
+// near 3 x num_sms x slots (profiles/r2_hybrid_threshold.txt).  The round-1
+// hub kernel needed 13x.
+constexpr int64_t kHybridMinEdgesPerSlot = 3;
 
 __global__ void k_count_u32(int64_t m, const uint32_t *__restrict__ ids, uint32_t *__restrict__ cnt) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
