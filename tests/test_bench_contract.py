@@ -51,9 +51,9 @@ def test_reference_arm_times_whole_calls():
     assert "x 10 iterations" in cb["sample"]
     assert d["config"]["iterations_per_step"] == 10
     assert cb["ms_per_iteration"] > 0 and cb["ms_setup_per_call"] >= 0
-    # value = |E| x iterations / step time (ms_per_step is printed to 4 decimals)
+    # value = |E| x iterations / step time (printed rounded: ms to 4, value to 3 decimals)
     want = 16 * 4096 * 10 / (d["ms_per_step"] / 1e3) / 1e9
-    assert abs(d["value"] - want) <= (1e-3 + 1e-4 / d["ms_per_step"]) * d["value"] + 1e-6
+    assert abs(d["value"] - want) <= (1e-3 + 1e-4 / d["ms_per_step"]) * d["value"] + 5e-4
 
 
 def test_gpus_flag_must_match_world():
