@@ -109,7 +109,21 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const unsigned FULL = 0xffffffffu;
   const int64_t stride = (int64_t)gridDim.x * NW;
 
-  for (int i = threadIdx.x; i < hot; i += blockDim.x) s_hot[i] = __ldcg(hot_src + i);
+  // stage the hot table: 8 loads in flight per thread (one at a time, the
+  // ~15 rounds of a 1024-thread CTA each waited a full L2/DRAM latency)
+  for (int i0 = threadIdx.x; i0 < hot; i0 += 8 * blockDim.x) {
+    double x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = i0 + j * blockDim.x;
+      x[j] = i < hot ? __ldcg(hot_src + i) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = i0 + j * blockDim.x;
+      if (i < hot) s_hot[i] = x[j];
+    }
+  }
   __syncthreads();
 
   int64_t t = (int64_t)blockIdx.x * NW + wid;

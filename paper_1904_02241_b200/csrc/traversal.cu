@@ -558,8 +558,11 @@ int gcb_bfs(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t source
     DArray<uint32_t> levels(g->n ? g->n : 1);
     std::vector<int64_t> sizes;
     std::vector<uint8_t> dirs;
-    bfs_run(ctx, g, bg, source, mode, capacity_bytes, value_bytes, depth.p, levels.p, sizes, dirs,
-            level_verts_host);
+    {
+      ProfScope ps(ctx, 3);  // device span of the traversal (bench.py ms_device)
+      bfs_run(ctx, g, bg, source, mode, capacity_bytes, value_bytes, depth.p, levels.p, sizes,
+              dirs, level_verts_host);
+    }
     d2h(ctx, depth_host, depth.p, g->n);
     sync(ctx);
     if (level_verts_host) GCB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
@@ -598,6 +601,9 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
   DArray<int64_t> dist(n ? n : 1);
   DArray<uint32_t> queue(n ? n : 1);
   Frontier F(n);
+  int64_t qsize = 1, r = 0;
+  {
+  ProfScope ps(ctx, 3);  // device span of the traversal (bench.py ms_device)
   k_fill_i64<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, kInfDist, dist.p);
   after_launch(ctx, "k_fill_i64");
   GCB_CUDA(cudaMemsetAsync(F.next.p, 0, F.next.n, ctx->stream));
@@ -610,7 +616,6 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
     h2d(ctx, F.bits.p + (source >> 5), &bit, 1);
     sync(ctx);
   }
-  int64_t qsize = 1, r = 0;
   uint64_t work;
   {
     int64_t h[2];
@@ -654,6 +659,7 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
     work = ds;
     ++r;
   }
+  }
   d2h(ctx, dist_host, dist.p, n);
   sync(ctx);
   *rounds = r;
@@ -667,6 +673,8 @@ int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_c
   const int64_t n = g->n;
   DArray<uint32_t> parent(n ? n : 1);
   DArray<unsigned long long> cnt(1);
+  {
+  ProfScope ps(ctx, 3);  // device span of the labelling (bench.py ms_device)
   GCB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
   k_cc_init<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, parent.p);
   after_launch(ctx, "k_cc_init");
@@ -689,6 +697,7 @@ int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_c
   }
   k_cc_compress<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, parent.p, cnt.p);
   after_launch(ctx, "k_cc_compress");
+  }
   unsigned long long hc = 0;
   d2h(ctx, labels_host, parent.p, n);
   d2h(ctx, &hc, cnt.p, 1);
