@@ -228,15 +228,17 @@ def workload_config(args, n, m, world):
                    "untimed warm-up (e2e: hot-bit layout of each freshly uploaded graph)"
                    if world == 1 and not args.exact and not args.f32_values else
                    "degree-ordered shards: graph renumbered by out-degree on every rank, slabs "
-                   "blocked with the prefix hot set (gcb_shard_blocking)"
+                   "blocked with the prefix hot set and the hub pass where it pays "
+                   "(gcb_shard_blocking); intermediate steps skip ids without out-edges"
                    if world > 1 and not args.exact and not args.f32_values
-                   and os.environ.get("GCB_SHARD_ORDER", "0") == "1" else
+                   and os.environ.get("GCB_SHARD_ORDER", "1") == "1" else
                    "as built by the call path (no promotion)"),
         "iterations_per_step": args.iters, "damping": 0.85, "tol": 0.0,
         "direction": args.direction, "value_dtype": "f32" if args.f32_values else "f64",
         "l2": "inputs larger than L2 (col arena 4|E| bytes >> 126 MB)",
-        "parallelism": (f"destination shards x{world} (cuts balance in-edges + 4 x vertices), "
-                        "contribution exchange per config.exchange" if world > 1 else "single GPU"),
+        "parallelism": (f"destination shards x{world} (cuts balance in-edges + 4 x live "
+                        "vertices, then one re-cut from measured steps), contribution exchange "
+                        "per config.exchange" if world > 1 else "single GPU"),
     }
 
 
@@ -292,28 +294,66 @@ def run_ours(args):
 
         if args.direction != "pull":
             raise SystemExit("multi-GPU PageRank shards the pull direction")
-        # GCB_SHARD_ORDER=1: every rank renumbers the graph by out-degree and
-        # blocks its slab with the global prefix hot set.  Off by default: at
-        # rmat:24, P = 8 the slab-local hot sets of the original numbering ran
-        # every shard step faster (max 0.144 vs 0.149 ms, DESIGN 7)
+        # every rank renumbers the graph by out-degree and blocks its slab with
+        # the global prefix hot set (and the hub pass where it pays); the cuts
+        # charge vertex cost to live rows only, since intermediate tol = 0 steps
+        # skip the ids without out-edges.  At rmat:24, P = 8 that ran the
+        # slowest shard step in 0.118 ms against 0.145 ms for the input
+        # numbering (DESIGN 7).  GCB_SHARD_ORDER=0 keeps the input numbering.
         ordered = (not args.exact and not args.f32_values
-                   and os.environ.get("GCB_SHARD_ORDER", "0") == "1")
+                   and os.environ.get("GCB_SHARD_ORDER", "1") == "1")
+        live = None
         if ordered:
             src, _perm = parallel.degree_order(src)
-        plan = parallel.ShardPlan(parallel.shard_ranges(src.row_offsets, world))
-        # width 0: size each shard's blocks from the sources its slab reads
-        engine = parallel.DeviceShard(src, *plan.owned(rank), 0, flags, ordered)
-        # default: the exchange fused into the rank update over peer memory
-        # (csrc/exchange.cu); GCB_EXCHANGE=nccl selects the sparse NCCL
-        # all_to_all, which is also the fallback when peer mapping fails
-        exchange = None
-        if os.environ.get("GCB_EXCHANGE", "p2p") == "p2p":
-            try:
-                exchange = parallel.PeerExchange(engine, plan, rank)
-            except RuntimeError as e:
-                print(f"peer exchange unavailable ({e}); using NCCL all_to_all", file=sys.stderr)
-        if exchange is None:
-            exchange = parallel.SparseExchange(plan, rank, engine.source_mask())
+            live = parallel.live_end(src)
+
+        def build(ranges):
+            plan = parallel.ShardPlan(ranges)
+            # width 0: size each shard's blocks from the sources its slab reads
+            engine = parallel.DeviceShard(src, *plan.owned(rank), 0, flags, ordered)
+            # default: the exchange fused into the rank update over peer memory
+            # (csrc/exchange.cu); GCB_EXCHANGE=nccl selects the sparse NCCL
+            # all_to_all, which is also the fallback when peer mapping fails
+            exchange = None
+            if os.environ.get("GCB_EXCHANGE", "p2p") == "p2p":
+                try:
+                    exchange = parallel.PeerExchange(engine, plan, rank)
+                except RuntimeError as e:
+                    print(f"peer exchange unavailable ({e}); using NCCL all_to_all",
+                          file=sys.stderr)
+            if exchange is None:
+                exchange = parallel.SparseExchange(plan, rank, engine.source_mask())
+            return plan, engine, exchange
+
+        ranges = parallel.shard_ranges(src.row_offsets, world, live_end=live)
+        plan, engine, exchange = build(ranges)
+        if os.environ.get("GCB_SHARD_CALIB", "1") == "1":
+            # one calibration pass (untimed setup): every rank times its own
+            # intermediate step, the cuts move to the measured costs
+            # (parallel.rebalance_ranges), and the shards are rebuilt
+            import torch.distributed as dist
+
+            c = torch.zeros(src.num_vertices, dtype=torch.float64, device=engine.device)
+            r_ = torch.zeros_like(c)
+            engine.init(c, r_)
+            for _ in range(3):
+                engine.step(c, r_, 0.85, False, dead_skip=True)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                engine.step(c, r_, 0.85, False, dead_skip=True)
+            e1.record()
+            torch.cuda.synchronize()
+            times = [None] * world
+            dist.all_gather_object(times, e0.elapsed_time(e1) / 5)
+            del c, r_
+            if getattr(exchange, "close", None):
+                exchange.close()
+            del engine, exchange
+            ranges = parallel.rebalance_ranges(src.row_offsets, ranges, times, live_end=live)
+            plan, engine, exchange = build(ranges)
         runner = parallel.ShardedPageRank(engine, plan, rank, exchange)
         n, m = src.num_vertices, src.num_edges
         bg = engine.bg

@@ -56,6 +56,9 @@ extern "C" {
 #define GCB_FLAG_NO_L2_WINDOW 4u /* disable the per-block access-policy window */
 #define GCB_FLAG_NO_GRAPH 8u     /* launch eagerly instead of a CUDA graph     */
 #define GCB_FLAG_NO_RELABEL 16u  /* fast pull paths: keep the input numbering  */
+#define GCB_FLAG_DEAD_SKIP 32u   /* shard steps on degree-ordered shards, tol = 0,
+                                    not the last iteration: ranks and delta are
+                                    dead, update only owned ids with out-edges */
 
 /* BFS direction modes (DirectionPolicy.MODES, traversal.py:46-61) */
 #define GCB_BFS_AUTO 0

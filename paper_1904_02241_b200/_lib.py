@@ -24,6 +24,7 @@ FLAG_F32_VALUES = 2
 FLAG_NO_L2_WINDOW = 4
 FLAG_NO_GRAPH = 8
 FLAG_NO_RELABEL = 16
+FLAG_DEAD_SKIP = 32
 BFS_AUTO, BFS_FORCE_PUSH, BFS_FORCE_PULL = 0, 1, 2
 
 c_i64 = ctypes.c_int64

@@ -319,7 +319,9 @@ int gcb_pr_shard_step_p2p(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1,
   DeviceGuard dg(ctx->device);
   ensure_derived(ctx, bg);
   bg->sums.ensure(bg->n);
-  const int64_t cnt = v1 - v0;
+  // dead-skip steps (GCB_FLAG_DEAD_SKIP): ids without out-edges are read by no
+  // slab (their need masks are 0), so their stores are skipped with them
+  const int64_t cnt = shard_live_range(ctx, bg, v0, v1, flags, deg_dev) - v0;
   const unsigned grid = grid_for((cnt + 3) / 4, 512, (int64_t)(1 << 20) * ctx->num_sms);
   bg->deltas.ensure((int64_t)grid + 2);
   check_peer_error(ctx);

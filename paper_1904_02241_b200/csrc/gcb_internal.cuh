@@ -222,6 +222,8 @@ struct gcb_blocked {
   int64_t n_live = -1;               // degree-ordered copies: ids [0, n_live) have out-degree
                                      // > 0 (the rest contribute 0 forever); -1 = not counted
   int64_t n_conn = 0;                // ... and [n_conn, n) are isolated (no edge either way)
+  bool dead_dirty = false;           // shard steps: sums of [n_live, v1) not cleared since a
+                                     // GCB_FLAG_DEAD_SKIP step (pr.cu shard_live_range)
   gcb_blocked *pending_hybrid = nullptr;  // build scratch of ensure_relabeled (owned)
   gcb_blocked *exact_pull = nullptr;      // push graphs: single-block pull blocking of the
                                           // transpose for the exact push (relabel.cu, owned)
@@ -362,6 +364,8 @@ bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters);
 gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg);
 gcb_blocked *ensure_exact_pull(gcb_ctx *ctx, gcb_blocked *bg);
 void permute_out(gcb_ctx *ctx, const gcb_blocked *bg, const double *y_new, double *y);
+int64_t shard_live_range(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, uint32_t flags,
+                         const uint32_t *deg_dev);
 int64_t hot_capacity(gcb_ctx *ctx);    // gather.cu: pull hot-table slots
 int64_t push_hot_slots(gcb_ctx *ctx);  // pr.cu: push hub-accumulator slots
 void destroy_pr_graph(struct ::PrGraph *g);  // pr.cu

@@ -1586,6 +1586,38 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   *conv = cv;
 }
 
+// Shard steps with GCB_FLAG_DEAD_SKIP on a degree-ordered shard (ids sorted by
+// descending out-degree: [n_live, n) have none): the step's ranks and delta
+// are dead, so only [v0, min(v1, n_live)) is updated; the sums of the rest are
+// then not cleared, and the next step without the flag (the last iteration)
+// clears them before its gather.  Returns the end of the range to update.
+int64_t shard_live_range(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, uint32_t flags,
+                         const uint32_t *deg_dev) {
+  const bool skip = (flags & GCB_FLAG_DEAD_SKIP) && bg->is_relabeled && !(flags & GCB_FLAG_EXACT);
+  if (skip || bg->dead_dirty) {
+    if (bg->n_live < 0) {
+      DArray<unsigned long long> cnt(1);
+      GCB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
+      k_count_nonzero_u32<<<grid_for(bg->n, 256, 4096), 256, 0, ctx->stream>>>(bg->n, deg_dev,
+                                                                                cnt.p);
+      after_launch(ctx, "k_count_nonzero_u32");
+      unsigned long long h = 0;
+      d2h(ctx, &h, cnt.p, 1);
+      sync(ctx);
+      bg->n_live = (int64_t)h;
+    }
+  }
+  const int64_t live = bg->n_live < 0 ? v1 : (bg->n_live < v0 ? v0 : (bg->n_live > v1 ? v1 : bg->n_live));
+  if (!skip) {
+    if (bg->dead_dirty && live < v1)
+      GCB_CUDA(cudaMemsetAsync(bg->sums.p + live, 0, (v1 - live) * sizeof(double), ctx->stream));
+    bg->dead_dirty = false;
+    return v1;
+  }
+  if (live < v1) bg->dead_dirty = true;
+  return live;
+}
+
 }  // namespace gcb
 
 using namespace gcb;
@@ -1850,7 +1882,9 @@ int gcb_pr_shard_step(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, dou
   DeviceGuard dg(ctx->device);
   ensure_derived(ctx, bg);
   bg->sums.ensure(bg->n);
-  const int64_t cnt = v1 - v0;
+  const int64_t u1 = shard_live_range(ctx, bg, v0, v1, flags, deg_dev);
+  const bool dead_skip = u1 < v1 || (flags & GCB_FLAG_DEAD_SKIP);
+  const int64_t cnt = u1 - v0;
   const unsigned grid = update_grid(ctx, cnt);
   bg->deltas.ensure((int64_t)grid + 2);
   // gather reads the full contribution vector, then the owned slice is
@@ -1864,7 +1898,8 @@ int gcb_pr_shard_step(gcb_ctx *ctx, gcb_blocked *bg, int64_t v0, int64_t v1, dou
     ProfScope ps(ctx, 2);
     launch_update(ctx, flags & GCB_FLAG_EXACT, cnt, (1.0 - damping) / (double)bg->n, damping,
                   bg->sums.p + v0, ranks_dev + v0, deg_dev + v0, contrib_dev + v0, nullptr,
-                  delta_dev ? bg->deltas.p : nullptr);  // no delta wanted: old ranks unread
+                  delta_dev ? bg->deltas.p : nullptr,  // no delta wanted: old ranks unread
+                  !(dead_skip && !delta_dev));         // dead-skip steps: ranks dead too
   }
   if (delta_dev) {
     if (cnt) {

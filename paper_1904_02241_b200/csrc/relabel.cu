@@ -464,6 +464,12 @@ __global__ void k_csr_edges(int64_t n, const int64_t *__restrict__ ro, const uin
   }
 }
 
+__global__ void k_nonempty_rows(int64_t n, const int64_t *__restrict__ ro, uint8_t *__restrict__ out) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    out[v] = ro[v + 1] > ro[v] ? 1 : 0;
+}
+
 static void csr_edge_list(gcb_ctx *ctx, const gcb_csr *g, const uint32_t *perm, uint32_t *rows,
                           uint32_t *cols) {
   if (!g->m) return;
@@ -494,6 +500,16 @@ int gcb_csr_degree_order(gcb_ctx *ctx, const gcb_csr *gt, uint32_t *perm_dev, gc
       after_launch(ctx, "k_count_u32");
     }
     if (n) {
+      // the same key as ensure_relabeled: vertices with in-edges only before
+      // isolated ones (a transpose row is a destination's in-edges)
+      DArray<uint8_t> has_in(n);
+      DArray<unsigned long long> cnt(2);
+      GCB_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
+      k_nonempty_rows<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, gt->ro.p, has_in.p);
+      after_launch(ctx, "k_nonempty_rows");
+      k_order_keys<<<grid_for(n, 256, 4096), 256, 0, ctx->stream>>>(n, k1.p, has_in.p, k2.p, cnt.p);
+      after_launch(ctx, "k_order_keys");
+      std::swap(k1, k2);
       k_iota_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, v1.p);
       after_launch(ctx, "k_iota_u32");
       uint32_t *rk = nullptr, *inv = nullptr;

@@ -45,9 +45,11 @@ VERTEX_COST = 4.0
 
 
 def shard_ranges(row_offsets, parts: int, align: int = 4,
-                 vertex_cost: float = VERTEX_COST) -> np.ndarray:
+                 vertex_cost: float = VERTEX_COST, live_end: int | None = None) -> np.ndarray:
     """Split rows into ``parts`` contiguous ranges of ~equal cost, cost =
     in-edges + vertex_cost * rows (vertex_cost=0: equal edge counts).
+    ``live_end``: rows at or past it (degree-ordered ids without out-edges,
+    which dead-skip steps do not update) carry no vertex cost.
 
     Boundaries are multiples of ``align`` (the update kernel's vector width)
     except the last, which is num_rows.  Returns int64[parts + 1]."""
@@ -55,12 +57,50 @@ def shard_ranges(row_offsets, parts: int, align: int = 4,
     n = ro.size - 1
     if parts < 1:
         raise ValueError("parts must be >= 1")
-    cost = ro.astype(np.float64) + float(vertex_cost) * np.arange(n + 1, dtype=np.float64)
+    rows = np.arange(n + 1, dtype=np.float64)
+    if live_end is not None:
+        rows = np.minimum(rows, float(live_end))
+    cost = ro.astype(np.float64) + float(vertex_cost) * rows
     total = float(cost[-1])
     cuts = [0]
     for r in range(1, parts):
         target = total * r / parts
         v = int(np.searchsorted(cost, target, side="left"))
+        v = min(n, max(cuts[-1], (v // align) * align))
+        cuts.append(v)
+    cuts.append(n)
+    return np.asarray(cuts, dtype=np.int64)
+
+
+def rebalance_ranges(row_offsets, ranges, step_ms, align: int = 4,
+                     vertex_cost: float = VERTEX_COST, live_end: int | None = None) -> np.ndarray:
+    """One calibration pass of the cuts: each shard's measured step time over
+    its model cost (in-edges + vertex_cost * live rows) gives a time density
+    for its rows, and the rows are re-cut into equal shares of the resulting
+    time.  The model misses what differs between shards -- at rmat:24 the
+    degree-ordered shards holding the hub destinations run most of their
+    edges through the cheaper hub pass -- and one pass moves the cuts to the
+    measured costs."""
+    ro = np.asarray(row_offsets, dtype=np.int64)
+    n = ro.size - 1
+    ranges = np.asarray(ranges, dtype=np.int64)
+    parts = ranges.size - 1
+    rows = np.arange(n + 1, dtype=np.float64)
+    if live_end is not None:
+        rows = np.minimum(rows, float(live_end))
+    cost = ro.astype(np.float64) + float(vertex_cost) * rows
+    dens = np.empty(parts)
+    for r in range(parts):
+        c = cost[ranges[r + 1]] - cost[ranges[r]]
+        dens[r] = float(step_ms[r]) / c if c > 0 else 0.0
+    # time-weighted cumulative cost: per-row increments scaled by their shard's density
+    inc = np.diff(cost)
+    owner = np.searchsorted(ranges[1:], np.arange(n), side="right")
+    tcum = np.concatenate([[0.0], np.cumsum(inc * dens[owner])])
+    total = float(tcum[-1])
+    cuts = [0]
+    for r in range(1, parts):
+        v = int(np.searchsorted(tcum, total * r / parts, side="left"))
         v = min(n, max(cuts[-1], (v // align) * align))
         cuts.append(v)
     cuts.append(n)
@@ -377,6 +417,20 @@ def degree_order(gt: CsrGraph):
     return CsrGraph._from_device(ctx, raw), perm[:gt.num_vertices]
 
 
+def live_end(gt: CsrGraph) -> int:
+    """Number of ids with out-edges of a degree-ordered transpose (they are
+    [0, live_end)): the vertices a dead-skip shard step updates."""
+    import torch
+
+    h = gt.device()
+    ctx = h.ctx
+    deg = torch.empty(max(gt.num_vertices, 1), dtype=torch.int32,
+                      device=torch.device("cuda", ctx.device))
+    _lib.check(ctx._lib.gcb_csr_col_counts(ctx.handle, h.raw, ctypes.c_void_p(deg.data_ptr())),
+               "col counts")
+    return int((deg[:gt.num_vertices] != 0).sum())
+
+
 def unpermute(values_new, perm):
     """values in the original numbering: out[v] = values_new[perm[v]]."""
     return values_new[perm.long()]
@@ -474,10 +528,18 @@ class DeviceShard:
             ctypes.c_void_p(ex.out_tab[epoch % 2].data_ptr()), ctypes.c_void_p(ex.need.data_ptr()),
             P, ex.rank, ctypes.c_void_p(ex.flag_tab.data_ptr()), epoch & 0xFFFFFFFF), "shard init p2p")
 
-    def step_p2p(self, ranks, ex: PeerExchange, epoch: int, damping: float, want_delta: bool):
+    def _flags(self, dead_skip: bool) -> int:
+        # GCB_FLAG_DEAD_SKIP: the step's ranks and delta are dead (tol = 0, not
+        # the last iteration); degree-ordered shards then update only owned ids
+        # with out-edges (csrc/pr.cu shard_live_range)
+        return self.flags | (_lib.FLAG_DEAD_SKIP if dead_skip and self.degree_ordered else 0)
+
+    def step_p2p(self, ranks, ex: PeerExchange, epoch: int, damping: float, want_delta: bool,
+                 dead_skip: bool = False):
         P = ex.plan.parts
         _lib.check(self.ctx._lib.gcb_pr_shard_step_p2p(
-            self.ctx.handle, self.bg.device().raw, self.v0, self.v1, float(damping), self.flags,
+            self.ctx.handle, self.bg.device().raw, self.v0, self.v1, float(damping),
+            self._flags(dead_skip and not want_delta),
             ctypes.c_void_p(self.deg.data_ptr()), ctypes.c_void_p(ex.buffer(epoch - 1)),
             ctypes.c_void_p(ranks.data_ptr()),
             ctypes.c_void_p(self.delta.data_ptr()) if want_delta else None,
@@ -486,9 +548,10 @@ class DeviceShard:
             epoch & 0xFFFFFFFF), "shard step p2p")
         return self.delta if want_delta else None
 
-    def step(self, contrib, ranks, damping: float, want_delta: bool):
+    def step(self, contrib, ranks, damping: float, want_delta: bool, dead_skip: bool = False):
         _lib.check(self.ctx._lib.gcb_pr_shard_step(
-            self.ctx.handle, self.bg.device().raw, self.v0, self.v1, float(damping), self.flags,
+            self.ctx.handle, self.bg.device().raw, self.v0, self.v1, float(damping),
+            self._flags(dead_skip and not want_delta),
             ctypes.c_void_p(self.deg.data_ptr()), ctypes.c_void_p(contrib.data_ptr()),
             ctypes.c_void_p(ranks.data_ptr()),
             ctypes.c_void_p(self.delta.data_ptr()) if want_delta else None), "shard step")
@@ -516,8 +579,9 @@ class ShardedPageRank:
         eng.init(contrib, ranks)
         self.exchange.sync(contrib)
         it, conv = 0, False
-        for _ in range(params.max_iters):
-            d = eng.step(contrib, ranks, params.damping, params.tol > 0.0)
+        for k in range(params.max_iters):
+            d = eng.step(contrib, ranks, params.damping, params.tol > 0.0,
+                         dead_skip=params.tol == 0.0 and k < params.max_iters - 1)
             self.exchange.sync(contrib)
             it += 1
             if params.tol > 0.0:
@@ -540,9 +604,10 @@ class ShardedPageRank:
         e = ex.begin()
         eng.init_p2p(ranks, ex, e)
         it, conv = 0, False
-        for _ in range(params.max_iters):
+        for k in range(params.max_iters):
             e += 1
-            d = eng.step_p2p(ranks, ex, e, params.damping, params.tol > 0.0)
+            d = eng.step_p2p(ranks, ex, e, params.damping, params.tol > 0.0,
+                             dead_skip=params.tol == 0.0 and k < params.max_iters - 1)
             it += 1
             if params.tol > 0.0:
                 if ex.allreduce_sum(float(d.item()), eng.device) < params.tol:
@@ -610,9 +675,11 @@ def sharded_pagerank_virtual(gt: CsrGraph, parts: int, width: int,
     import torch
 
     perm = None
+    live = None
     if degree_ordered:
         gt, perm = degree_order(gt)
-    plan = ShardPlan(shard_ranges(gt.row_offsets, parts))
+        live = live_end(gt)
+    plan = ShardPlan(shard_ranges(gt.row_offsets, parts, live_end=live))
     flags = _lib.FLAG_EXACT if exact else 0
     shards = [DeviceShard(gt, *plan.owned(r), width, flags, degree_ordered)
               for r in range(parts)]
@@ -625,8 +692,9 @@ def sharded_pagerank_virtual(gt: CsrGraph, parts: int, width: int,
         s.init(c, r)
     ex.sync_all(contribs)
     it, conv = 0, False
-    for _ in range(params.max_iters):
-        deltas = [s.step(c, r, params.damping, params.tol > 0.0)
+    for k in range(params.max_iters):
+        dead = params.tol == 0.0 and k < params.max_iters - 1
+        deltas = [s.step(c, r, params.damping, params.tol > 0.0, dead_skip=dead)
                   for s, c, r in zip(shards, contribs, ranks)]
         ex.sync_all(contribs)
         it += 1

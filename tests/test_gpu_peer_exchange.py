@@ -52,6 +52,19 @@ def _worker(rank, world, port, out_dir):
         # sharded SpMV over the same slabs, y all-gathered across the processes
         x = torch.as_tensor(np.random.default_rng(9).random(gt.num_vertices)).cuda()
         results[f"spmv_{exact}"] = parallel.ShardedSpmv(eng, plan, rank).run(x).cpu().numpy()
+    # degree-ordered shards (fast): intermediate tol = 0 steps skip the ids
+    # without out-edges (GCB_FLAG_DEAD_SKIP), cuts by live vertex cost
+    gdo, perm = parallel.degree_order(gt)
+    plan_do = parallel.ShardPlan(parallel.shard_ranges(gdo.row_offsets, world,
+                                                       live_end=parallel.live_end(gdo)))
+    eng = parallel.DeviceShard(gdo, *plan_do.owned(rank), 0, 0, True)
+    ex = parallel.PeerExchange(eng, plan_do, rank)
+    runner = parallel.ShardedPageRank(eng, plan_do, rank, ex)
+    for rep in range(2):
+        for iters in (1, 10):
+            r = runner.run(gcb.PrParams(tol=0.0, max_iters=iters))
+            results[f"do{iters}_{rep}"] = parallel.unpermute(r.ranks, perm).cpu().numpy()
+    ex.close()
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **results)
     dist.destroy_process_group()
 
@@ -68,6 +81,7 @@ def test_peer_exchange_matches_unsharded(tmp_path, world):
     _, scale, ef, seed = GRAPH
     bg = gcb.partition_tocab(gcb.generate_rmat(scale, ef, seed, transposed=True), "pull", 1 << 12)
     want = gcb.pr_blocked(bg, gcb.PrParams(tol=0.0, max_iters=10), exact=True).ranks
+    want1 = gcb.pr_blocked(bg, gcb.PrParams(tol=0.0, max_iters=1), exact=True).ranks
     want_tol = gcb.pr_blocked(bg, gcb.PrParams(tol=1e-9, max_iters=200), exact=True)
     want_y = gcb.spmv_blocked(bg, np.random.default_rng(9).random(bg.num_vertices), exact=True)
     for rank in range(world):
@@ -75,6 +89,8 @@ def test_peer_exchange_matches_unsharded(tmp_path, world):
         for rep in range(2):
             assert np.array_equal(got[f"p10_True_{rep}"], want)
             assert np.max(np.abs(got[f"p10_False_{rep}"] - want) / want) <= 1e-12
+            assert np.max(np.abs(got[f"do10_{rep}"] - want) / want) <= 1e-12
+            assert np.max(np.abs(got[f"do1_{rep}"] - want1) / want1) <= 1e-12
         it, conv = got["tol_True_it"]
         assert (int(it), bool(conv)) == (want_tol.iterations, want_tol.converged)
         assert np.array_equal(got["tol_True"], want_tol.ranks)

@@ -31,6 +31,36 @@ def test_shard_ranges_balance_cost():
         assert cost.max() / cost.mean() < 1.05, cost
 
 
+def test_shard_ranges_live_end():
+    # rows past live_end (degree-ordered ids without out-edges) carry no vertex
+    # cost: with every row dead the cuts are equal edge counts
+    g = orc.rmat_transpose(14, 16, 1)
+    vc = parallel.VERTEX_COST
+    for parts in (2, 4, 8):
+        assert np.array_equal(parallel.shard_ranges(g.row_offsets, parts, live_end=0),
+                              parallel.shard_ranges(g.row_offsets, parts, vertex_cost=0.0))
+        assert np.array_equal(parallel.shard_ranges(g.row_offsets, parts, live_end=g.n),
+                              parallel.shard_ranges(g.row_offsets, parts))
+        live = g.n // 3
+        cuts = parallel.shard_ranges(g.row_offsets, parts, live_end=live)
+        rows_live = np.diff(np.minimum(cuts, live))
+        cost = np.diff(g.row_offsets[cuts]) + vc * rows_live
+        assert cost.max() / cost.mean() < 1.1, cost  # hub rows limit the granularity
+
+
+def test_rebalance_ranges():
+    # a shard measured twice as slow per model cost gets ~half the rows' cost
+    g = orc.rmat_transpose(14, 16, 1)
+    cuts = parallel.shard_ranges(g.row_offsets, 4, vertex_cost=0.0)
+    same = parallel.rebalance_ranges(g.row_offsets, cuts, [1.0, 1.0, 1.0, 1.0], vertex_cost=0.0)
+    assert np.abs(same - cuts).max() <= 4
+    new = parallel.rebalance_ranges(g.row_offsets, cuts, [2.0, 1.0, 1.0, 1.0], vertex_cost=0.0)
+    e_old = np.diff(g.row_offsets[cuts])
+    e_new = np.diff(g.row_offsets[new])
+    assert e_new[0] < 0.75 * e_old[0] and new[0] == 0 and new[-1] == g.n
+    assert all(c % 4 == 0 for c in new[:-1]) and (np.diff(new) >= 0).all()
+
+
 def test_shard_ranges_equal_edges():
     g = orc.rmat_transpose(14, 16, 1)
     for parts in (1, 2, 3, 4, 8):
@@ -81,7 +111,8 @@ class OracleShard:
         np.divide(np.full(self.v1 - self.v0, r0), d, out=c, where=d > 0)
         contrib[sl] = torch.from_numpy(c)
 
-    def step(self, contrib, ranks, damping, want_delta):
+    def step(self, contrib, ranks, damping, want_delta, dead_skip=False):
+        # dead_skip only allows skipping dead work; updating everything is exact
         c = contrib.numpy()
         sums = orc.gather_rows(c, self.col, self.ro)
         base = (1.0 - damping) / self.n
