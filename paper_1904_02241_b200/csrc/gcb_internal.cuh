@@ -222,6 +222,8 @@ struct gcb_blocked {
   int64_t n_live = -1;               // degree-ordered copies: ids [0, n_live) have out-degree
                                      // > 0 (the rest contribute 0 forever); -1 = not counted
   int64_t n_conn = 0;                // ... and [n_conn, n) are isolated (no edge either way)
+  const void *iso_clean[2] = {nullptr, nullptr};  // contrib / sums buffers whose isolated
+                                     // tail [n_conn, n) is known to be zero (pr.cu pr_run)
   bool dead_dirty = false;           // shard steps: sums of [n_live, v1) not cleared since a
                                      // GCB_FLAG_DEAD_SKIP step (pr.cu shard_live_range)
   gcb_blocked *pending_hybrid = nullptr;  // build scratch of ensure_relabeled (owned)

@@ -1476,23 +1476,19 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   const double base = (1.0 - damping) / (double)n;
   double *contrib = f32 ? nullptr : bg->contrib.p;
   float *contrib32 = f32 ? bg->contrib32.p : nullptr;
-  {
-    ProfScope ps(ctx, 3);
-    k_pr_init<<<upd_grid, 256, 0, ctx->stream>>>(n, r0, deg, tol > 0.0 ? ranks_dev : nullptr,
-                                                 contrib ? contrib : bg->contrib.p, contrib32,
-                                                 bg->sums.p);
-    after_launch(ctx, "k_pr_init");
-  }
   // Live range of the degree-ordered copy.  Its ids are sorted by descending
   // out-degree, so [n_live, n) is every vertex with out-degree 0: its
   // contribution is 0 in every iteration (kernels.py:185-191), and with
   // tol == 0 its intermediate ranks are never read (no delta; only the last
   // iteration's ranks are returned).  Those iterations update [0, n_live)
   // only (rmat:24: 7.38M of 16.8M vertices -- most R-MAT vertices are
-  // isolated); the last one updates every vertex, after clearing the sums of
-  // [n_live, n), which the skipped updates did not clear.  The ranks are
-  // unchanged: the skipped work is dead.
-  int64_t n_upd = n;
+  // isolated); the last one updates the rest after clearing the sums the
+  // skipped updates did not clear.  [n_conn, n) are isolated vertices: their
+  // sums stay 0 and all share one rank, so the last update stops at n_conn + 1
+  // (permute_out fills them from that one value), and once a buffer pair has
+  // been initialised in full their zero contributions and sums are not
+  // rewritten.  The ranks are unchanged: the skipped work is dead.
+  int64_t n_upd = n, n_fin = n, n_init = n;
   if (bg->is_relabeled && tol == 0.0 && !exact && !push && !f32 && !deg_override) {
     if (bg->n_live < 0) {
       DArray<unsigned long long> cnt(1);
@@ -1505,7 +1501,24 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
       bg->n_live = (int64_t)h;
     }
     const char *lv = getenv("GCB_FULL_UPDATE");  // A/B knob: 1 updates every vertex
-    if (!(lv && lv[0] == '1')) n_upd = bg->n_live;
+    if (!(lv && lv[0] == '1')) {
+      n_upd = bg->n_live;
+      if (bg->n_conn > 0 && bg->n_conn < n) {
+        n_fin = bg->n_conn + 1;
+        if (bg->iso_clean[0] == bg->contrib.p && bg->iso_clean[1] == bg->sums.p) n_init = n_fin;
+      }
+    }
+  }
+  {
+    ProfScope ps(ctx, 3);
+    k_pr_init<<<grid_for((n_init + 3) / 4, 256, 1 << 20), 256, 0, ctx->stream>>>(
+        n_init, r0, deg, tol > 0.0 ? ranks_dev : nullptr, contrib ? contrib : bg->contrib.p,
+        contrib32, bg->sums.p);
+    after_launch(ctx, "k_pr_init");
+    if (n_init == n) {
+      bg->iso_clean[0] = bg->contrib.p;
+      bg->iso_clean[1] = bg->sums.p;
+    }
   }
   // one iteration's launches (no host synchronisation: also the graph body);
   // with_ranks = false only where the ranks and delta are dead (tol == 0, not
@@ -1529,7 +1542,7 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
     }
     {
       ProfScope ps(ctx, 2);
-      launch_update(ctx, exact, with_ranks ? n : n_upd, base, damping, bg->sums.p, ranks_dev, deg,
+      launch_update(ctx, exact, with_ranks ? n_fin : n_upd, base, damping, bg->sums.p, ranks_dev, deg,
                     contrib ? contrib : (push ? bg->contrib.p : nullptr), contrib32,
                     tol > 0.0 ? bg->deltas.p : nullptr, with_ranks);
     }
@@ -1544,8 +1557,9 @@ static void pr_run(gcb_ctx *ctx, gcb_blocked *bg, double damping, double tol, in
   const bool keep_ranks = kr && kr[0] == '1';
   for (int k = 0; k < max_iters; ++k) {
     const bool last = tol > 0.0 || k == max_iters - 1 || keep_ranks;
-    if (last && k > 0 && n_upd < n)
-      GCB_CUDA(cudaMemsetAsync(bg->sums.p + n_upd, 0, (n - n_upd) * sizeof(double), ctx->stream));
+    if (last && k > 0 && n_upd < n_fin)
+      GCB_CUDA(cudaMemsetAsync(bg->sums.p + n_upd, 0, (n_fin - n_upd) * sizeof(double),
+                               ctx->stream));
     iterate(last);
     ++it;
     if (tol > 0.0) {
