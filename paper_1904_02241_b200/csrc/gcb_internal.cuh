@@ -171,6 +171,8 @@ struct gcb_blocked {
   gcb::DArray<uint32_t> id_map;  // [L]
   gcb::DArray<uint32_t> col;     // [m + pad]
   gcb::DArray<double> w;         // [m] or empty
+  gcb::DArray<uint8_t> w8;       // [m + pad] byte copy of integral weights in [0, 255] (SSSP)
+  int w8_state = 0;              // 0 unknown, 1 built, -1 weights do not fit a byte
 
   // ---- derived, built once by ensure_derived() ----
   bool derived = false;

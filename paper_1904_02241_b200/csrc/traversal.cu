@@ -424,6 +424,140 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The pull round, pipelined (k_sssp_pull_tiles left every tile a chain of
+// dependent round trips -- col, bitmap word, dist, weight -- and ran 364 us per
+// rmat:24 block at 80% long-scoreboard stalls, IPC 0.86):
+//   * the next tile's arena words, row-start bits, first row and weights are
+//     loaded while this tile is processed;
+//   * weights come as one vector per lane: 8 bytes when the graph's weights
+//     are integers in [0, 255] (an execution copy, ensure_w8), else 64 bytes
+//     of f64 -- streamed for every edge instead of one scattered 8-byte load
+//     per frontier edge;
+//   * the 8 frontier tests, then the 8 dist loads, are issued before any is
+//     used.
+template <bool W8>
+__global__ void __launch_bounds__(256, 4)
+    k_sssp_pull_pipe(const uint32_t *__restrict__ col, const double *__restrict__ w,
+                     const uint8_t *__restrict__ w8, const uint32_t *__restrict__ rstart,
+                     const uint32_t *__restrict__ id_map_b, const uint32_t *__restrict__ tile_row,
+                     int64_t es, int64_t ee, int64_t t0, int64_t ntiles,
+                     const uint32_t *__restrict__ front_bits, long long *__restrict__ dist,
+                     uint8_t *__restrict__ next) {
+  constexpr int V = kTileV;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= ntiles) return;
+  auto load = [&](int64_t tt, uint32_t (&c)[V], uint32_t &fw, uint32_t &r0, uint64_t &wb,
+                  double (&wd)[V]) {
+    const int64_t abase = (t0 + tt) * kTileT;
+    const uint4 *cp = reinterpret_cast<const uint4 *>(col + abase + lane * V);
+    const uint4 ca = __ldcs(cp), cb = __ldcs(cp + 1);
+    c[0] = ca.x; c[1] = ca.y; c[2] = ca.z; c[3] = ca.w;
+    c[4] = cb.x; c[5] = cb.y; c[6] = cb.z; c[7] = cb.w;
+    fw = rstart[(abase >> 5) + (lane < 8 ? lane : 8)];
+    r0 = tile_row[tt];
+    if (W8) {
+      wb = __ldcs(reinterpret_cast<const unsigned long long *>(w8 + abase + lane * V));
+    } else {
+      const double2 *wp = reinterpret_cast<const double2 *>(w + abase + lane * V);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double2 x = __ldcs(wp + j);
+        wd[2 * j] = x.x;
+        wd[2 * j + 1] = x.y;
+      }
+    }
+  };
+  uint32_t c[V], fw, r0;
+  uint64_t wb = 0;
+  double wd[V];
+  load(t, c, fw, r0, wb, wd);
+  for (; t < ntiles; t += nw) {
+    const int64_t abase = (t0 + t) * kTileT;
+    const int64_t tn = t + nw;
+    uint32_t cn[V], fwn = 0, r0n = 0;
+    uint64_t wbn = 0;
+    double wdn[V];
+    if (tn < ntiles) load(tn, cn, fwn, r0n, wbn, wdn);
+    const int llo = es > abase ? (int)(es - abase) : 0;
+    const int lhi = ee - abase < kTileT ? (int)(ee - abase) : kTileT;
+    const TileBits tb = tile_bits(fw, llo, lhi, lane);
+    uint32_t fm = 0;  // frontier sources among the lane's valid edges
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const uint32_t u = c[k];
+      const uint32_t word = ((tb.vm >> k) & 1u) ? __ldg(front_bits + (u >> 5)) : 0u;
+      fm |= ((word >> (u & 31)) & 1u) << k;
+    }
+    long long du[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) du[k] = ((fm >> k) & 1u) ? __ldcg(dist + c[k]) : LLONG_MAX;
+    long long cand[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const long long wk = W8 ? (long long)((wb >> (8 * k)) & 0xffu) : (long long)wd[k];
+      cand[k] = du[k] != LLONG_MAX ? du[k] + wk : LLONG_MAX;
+    }
+    tile_reduce<long long>(
+        cand, tb, r0, lane, LLONG_MAX, [](long long a, long long b) { return a < b ? a : b; },
+        [&](uint32_t row, long long x, uint32_t) {
+          if (x == LLONG_MAX) return;
+          const uint32_t v = id_map_b[row];
+          if (x < dist[v]) {
+            const long long old = atomicMin(&dist[v], x);
+            if (x < old) next[v] = 1;
+          }
+        });
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      c[k] = cn[k];
+      if (!W8) wd[k] = wdn[k];
+    }
+    fw = fwn;
+    r0 = r0n;
+    wb = wbn;
+  }
+}
+
+__global__ void k_w8_check(int64_t m, const double *__restrict__ w, unsigned *__restrict__ bad) {
+  unsigned b = 0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double x = w[e];
+    b |= !(x >= 0.0 && x <= 255.0 && x == (double)(int)x);
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+__global__ void k_w8_copy(int64_t m, const double *__restrict__ w, uint8_t *__restrict__ w8) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    w8[e] = (uint8_t)(int)w[e];
+}
+
+// Byte copy of a blocking's weights when every weight is an integer in
+// [0, 255] (U[1, 255] at the configs[3] sizes); built once.
+static const uint8_t *ensure_w8(gcb_ctx *ctx, gcb_blocked *bg) {
+  if (bg->w8_state) return bg->w8_state > 0 ? bg->w8.p : nullptr;
+  bg->w8_state = -1;
+  if (!bg->weighted || bg->m == 0) return nullptr;
+  DArray<unsigned> bad(1);
+  GCB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned), ctx->stream));
+  k_w8_check<<<grid_for(bg->m, 256, 65536), 256, 0, ctx->stream>>>(bg->m, bg->w.p, bad.p);
+  after_launch(ctx, "k_w8_check");
+  unsigned h = 1;
+  d2h(ctx, &h, bad.p, 1);
+  sync(ctx);
+  if (h) return nullptr;
+  bg->w8.alloc(bg->m + kColPad);
+  GCB_CUDA(cudaMemsetAsync(bg->w8.p + bg->m, 0, kColPad, ctx->stream));
+  k_w8_copy<<<grid_for(bg->m, 256, 65536), 256, 0, ctx->stream>>>(bg->m, bg->w.p, bg->w8.p);
+  after_launch(ctx, "k_w8_copy");
+  bg->w8_state = 1;
+  return bg->w8.p;
+}
+
 // --------------------------------------------------------------------------
 // CC: lock-free union-find, always hooking the larger root under the smaller
 // one, so every final root is its component's minimum vertex id.
@@ -597,6 +731,7 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
                 "g_blocked must be a weighted pull blocking of g");
     ensure_row_bits(ctx, bg);
   }
+  const uint8_t *w8 = bg ? ensure_w8(ctx, bg) : nullptr;
   const int64_t n = g->n;
   DArray<int64_t> dist(n ? n : 1);
   DArray<uint32_t> queue(n ? n : 1);
@@ -642,12 +777,25 @@ int gcb_sssp(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg_pull, int64_t sourc
         const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
         if (!Lb) continue;
         const int64_t tb = bg->h_tile_base[b], nt = bg->h_tile_base[b + 1] - tb;
-        k_sssp_pull_tiles<<<grid_for(nt * 32, 256, (int64_t)ctx->num_sms * 8), 256, 0,
-                            ctx->stream>>>(bg->col.p, bg->w.p, bg->rstart.p, bg->id_map.p + rs,
-                                           bg->tile_row.p + tb, bg->h_edge_starts[b],
-                                           bg->h_edge_starts[b + 1], bg->h_tile_t0[b], nt,
-                                           F.bits.p, (long long *)dist.p, F.next.p);
-        after_launch(ctx, "k_sssp_pull_tiles");
+        const unsigned gsp = grid_for(nt * 32, 256, (int64_t)ctx->num_sms * 8);
+        const char *sp = getenv("GCB_SSSP_PULL");  // A/B knob: 0 = the round-1 kernel
+        if (sp && sp[0] == '0') {
+          k_sssp_pull_tiles<<<gsp, 256, 0, ctx->stream>>>(
+              bg->col.p, bg->w.p, bg->rstart.p, bg->id_map.p + rs, bg->tile_row.p + tb,
+              bg->h_edge_starts[b], bg->h_edge_starts[b + 1], bg->h_tile_t0[b], nt, F.bits.p,
+              (long long *)dist.p, F.next.p);
+        } else if (w8) {
+          k_sssp_pull_pipe<true><<<gsp, 256, 0, ctx->stream>>>(
+              bg->col.p, nullptr, w8, bg->rstart.p, bg->id_map.p + rs, bg->tile_row.p + tb,
+              bg->h_edge_starts[b], bg->h_edge_starts[b + 1], bg->h_tile_t0[b], nt, F.bits.p,
+              (long long *)dist.p, F.next.p);
+        } else {
+          k_sssp_pull_pipe<false><<<gsp, 256, 0, ctx->stream>>>(
+              bg->col.p, bg->w.p, nullptr, bg->rstart.p, bg->id_map.p + rs, bg->tile_row.p + tb,
+              bg->h_edge_starts[b], bg->h_edge_starts[b + 1], bg->h_tile_t0[b], nt, F.bits.p,
+              (long long *)dist.p, F.next.p);
+        }
+        after_launch(ctx, "k_sssp_pull");
       }
     }
     // compact next flags into the queue
