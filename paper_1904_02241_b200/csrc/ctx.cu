@@ -108,14 +108,24 @@ int gcb_ctx_create(int device, gcb_ctx **out) {
     }
     (void)cudaGetLastError();
   }
-  // Persisting L2 set-aside (for access-policy windows): opt-in only.
-  // Measured at scale 24 it slows every pass -- the rank update went from
-  // 0.12 to 0.24 ms per iteration and the gather from 0.92 to 1.00 ms -- while
-  // per-load L2::evict_last hints (createpolicy, ldst.cuh) keep the block's
-  // value slice resident without carving L2 (profiles/r1b_l2_policy.txt).
-  if (ctx->persist_max > 0 && getenv("GCB_L2_PERSIST")) {
-    cudaError_t le = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)ctx->persist_max);
-    if (le != cudaSuccess) (void)cudaGetLastError();
+  // Persisting L2 set-aside for the access-policy window of the pull gather
+  // (north star (1); gather.cu launch_block pins the head of the
+  // degree-ordered value slice).  48 MB: the set-aside sizes measured at
+  // rmat:24 (profiles/r2_l2_window_attr.txt) ran 7.186 ms per step at 48 MB
+  // against 7.19 ms for the per-load range policy without a set-aside, 7.25 at
+  // 32, 7.44 at 64 and 7.89 at the maximum (round 1's setting, which carved L2
+  // from every other pass).  GCB_L2_PERSIST=<MB> overrides (0: no set-aside,
+  // the per-load range policy; "max": the device maximum).
+  if (ctx->persist_max > 0) {
+    const char *env = getenv("GCB_L2_PERSIST");
+    const double mb = env && env[0] ? (strcmp(env, "max") == 0 ? -1.0 : atof(env)) : 48.0;
+    int64_t want = mb > 0 ? (int64_t)(mb * 1048576.0) : (mb < 0 ? ctx->persist_max : 0);
+    if (want > ctx->persist_max) want = ctx->persist_max;
+    if (want > 0) {
+      cudaError_t le = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)want);
+      if (le != cudaSuccess) (void)cudaGetLastError();
+      else ctx->persist_set = want;
+    }
   }
   *out = ctx;
   GCB_API_END

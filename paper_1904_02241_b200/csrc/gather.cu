@@ -64,18 +64,26 @@ __constant__ int c_abl;
 #define ABL(b) 0
 #endif
 
-template <bool HOTBIT>
+template <bool HOTBIT, bool HINT = true>
 __device__ __forceinline__ double gather_one(const double *vals, uint32_t c, uint32_t lo,
                                              uint32_t hot, uint32_t s_hot, uint64_t pol) {
   const uint32_t h = HOTBIT ? (c ^ kHotBit) : c - lo;
   double x;
   if (ABL(1) && h >= hot) return 0.0;
-  asm("{\n\t.reg .pred p;\n\t"
-      "setp.lt.u32 p, %1, %2;\n\t"
-      "@p ld.shared.f64 %0, [%3];\n\t"
-      "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%4], %5;\n\t}"
-      : "=d"(x)
-      : "r"(h), "r"(hot), "r"(s_hot + h * 8u), "l"(vals + c), "l"(pol));
+  if (HINT)
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.lt.u32 p, %1, %2;\n\t"
+        "@p ld.shared.f64 %0, [%3];\n\t"
+        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%4], %5;\n\t}"
+        : "=d"(x)
+        : "r"(h), "r"(hot), "r"(s_hot + h * 8u), "l"(vals + c), "l"(pol));
+  else  // no per-load policy: the launch's access-policy window governs L2
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.lt.u32 p, %1, %2;\n\t"
+        "@p ld.shared.f64 %0, [%3];\n\t"
+        "@!p ld.global.nc.L1::no_allocate.f64 %0, [%4];\n\t}"
+        : "=d"(x)
+        : "r"(h), "r"(hot), "r"(s_hot + h * 8u), "l"(vals + c));
   return x;
 }
 
@@ -89,7 +97,7 @@ struct RangePolicy {
   uint32_t keep, total;
 };
 
-template <bool WGT, bool ASSIGN, bool HOTBIT, int NW>
+template <bool WGT, bool ASSIGN, bool HOTBIT, int NW, bool HINT = true>
 __global__ void __launch_bounds__(NW * 32, 1)
     k_pull_hot(const uint32_t *__restrict__ col, const double *__restrict__ w,
                const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ id_map_b,
@@ -151,7 +159,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // gathers first: everything below overlaps their latency
     double v[V];
 #pragma unroll
-    for (int k = 0; k < V; ++k) v[k] = gather_one<HOTBIT>(vals, c[k], lo, (uint32_t)hot, s_hot_addr, pol_keep);
+    for (int k = 0; k < V; ++k)
+      v[k] = gather_one<HOTBIT, HINT>(vals, c[k], lo, (uint32_t)hot, s_hot_addr, pol_keep);
     if (WGT) {
       double ww[V];
       ld_stream_f64x4(w + abase + lane * V, pol_stream, ww);
@@ -521,19 +530,18 @@ static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double 
   int64_t grid = ceil_div(nt, kGWarps);
   if (grid > ctx->num_sms) grid = ctx->num_sms;
   const double *hot_src = HOTBIT ? bg->hotval.p + b * bg->hot_k : vals + lo;
-  // L2 residency window of the cold gathers (north star (1)): on the
-  // degree-ordered copy the block's value slice is sorted by out-degree, so
-  // its head holds the most-read cold values.  A range policy -- the
-  // per-instruction form of an access-policy window (createpolicy.range) --
-  // marks the first kL2KeepMB of the slice evict_last and leaves the tail at
-  // normal priority; at rmat:24 (64 MB slices) that ran 8.597 vs 8.610 ms per
-  // step against evict_last over the whole slice, and beat the launch-attribute
-  // window with a persisting set-aside (which carves L2 from every other
-  // pass, profiles/r1b_l2_policy.txt).  Marking the tail evict_first instead
-  // ran 8.650 ms; a 16 MB window 9.08 ms (profiles/r2_l2_window.txt).
-  // GCB_L2_RANGE="<MB>:<mode>" overrides (mode 1: tail evict_first, 2: tail
-  // unchanged, 0: whole slice evict_last); the hot-bit layout has no sorted
-  // slice and keeps evict_last.
+  // L2 residency of the cold gathers (north star (1)): on the degree-ordered
+  // copy the block's value slice is sorted by out-degree, so its head holds
+  // the most-read cold values.  With the context's persisting set-aside (48 MB
+  // by default, ctx.cu) the launch carries an access-policy window over that
+  // head (below).  Without one, a range policy -- the per-instruction form of
+  // the window (createpolicy.range) -- marks the first kL2KeepMB of the slice
+  // evict_last and leaves the tail at normal priority; the two ran 7.186 vs
+  // 7.19 ms per step at rmat:24 (profiles/r2_l2_window_attr.txt).  For the
+  // range policy, marking the tail evict_first ran slower, as did a 16 MB head
+  // (profiles/r2_l2_window.txt).  GCB_L2_RANGE="<MB>:<mode>" overrides it (mode
+  // 1: tail evict_first, 2: tail unchanged, 0: whole slice evict_last); the
+  // hot-bit layout has no sorted slice and keeps evict_last.
   RangePolicy rp{0, 0, 0};
   {
     double mb = kL2KeepMB;
@@ -547,11 +555,44 @@ static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double 
     if (mode && keep < total && total < (uint64_t(1) << 32))
       rp = RangePolicy{mode, (uint32_t)keep, (uint32_t)total};
   }
-  k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps>
-      <<<(unsigned)(grid < 1 ? 1 : grid), kGWarps * 32, smem, ctx->stream>>>(
-          HOTBIT ? bg->xcol.p : bg->col.p, WGT ? bg->w.p : nullptr, bg->rstart.p,
-          bg->id_map.p + rs, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt, (uint32_t)lo, hot,
-          (uint32_t)Lb, hot_src, vals, out, rp);
+  // North star (1): with a persisting set-aside in force (GCB_L2_PERSIST=<MB>)
+  // the head of a degree-ordered value slice -- its most-read cold values --
+  // is pinned by a launch access-policy window instead of the per-load range
+  // policy (measured against it in profiles/r2_l2_window_attr.txt).
+  const bool window = !HOTBIT && ctx->persist_set > 0 && ctx->window_max > 0;
+  if (window) {
+    uint64_t wbytes = (uint64_t)(hi - lo) * 8u;
+    if (wbytes > (uint64_t)ctx->persist_set) wbytes = (uint64_t)ctx->persist_set;
+    if (wbytes > (uint64_t)ctx->window_max) wbytes = (uint64_t)ctx->window_max;
+    ensure_smem_attrs(ctx, (const void *)k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps, false>, smem,
+                      pct > 100 ? 100 : pct);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(grid < 1 ? 1 : grid));
+    cfg.blockDim = dim3(kGWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = const_cast<double *>(vals + lo);
+    attr[0].val.accessPolicyWindow.num_bytes = (size_t)wbytes;
+    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GCB_CUDA(cudaLaunchKernelEx(&cfg, k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps, false>,
+                                (const uint32_t *)(HOTBIT ? bg->xcol.p : bg->col.p),
+                                (const double *)(WGT ? bg->w.p : nullptr),
+                                (const uint32_t *)bg->rstart.p, (const uint32_t *)(bg->id_map.p + rs),
+                                (const uint32_t *)(bg->tile_row.p + tb), es, ee, bg->h_tile_t0[b], nt,
+                                (uint32_t)lo, hot, (uint32_t)Lb, hot_src, vals, out, rp));
+  } else {
+    k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps>
+        <<<(unsigned)(grid < 1 ? 1 : grid), kGWarps * 32, smem, ctx->stream>>>(
+            HOTBIT ? bg->xcol.p : bg->col.p, WGT ? bg->w.p : nullptr, bg->rstart.p,
+            bg->id_map.p + rs, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt, (uint32_t)lo,
+            hot, (uint32_t)Lb, hot_src, vals, out, rp);
+  }
   after_launch(ctx, "k_pull_hot");
 }
 

@@ -114,6 +114,7 @@ struct gcb_ctx {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   int64_t l2_bytes = 0, persist_max = 0, window_max = 0;
+  int64_t persist_set = 0;  // persisting-L2 set-aside in force (GCB_L2_PERSIST), bytes
   int64_t launches = 0;
   void *pinned = nullptr;  // small pinned host staging (scalars)
   cudaStream_t copy_stream = nullptr;  // host->device copies overlapped with kernels
