@@ -108,17 +108,18 @@ int gcb_ctx_create(int device, gcb_ctx **out) {
     }
     (void)cudaGetLastError();
   }
-  // Persisting L2 set-aside for the access-policy window of the pull gather
-  // (north star (1); gather.cu launch_block pins the head of the
-  // degree-ordered value slice).  48 MB: the set-aside sizes measured at
-  // rmat:24 (profiles/r2_l2_window_attr.txt) ran 7.186 ms per step at 48 MB
-  // against 7.19 ms for the per-load range policy without a set-aside, 7.25 at
-  // 32, 7.44 at 64 and 7.89 at the maximum (round 1's setting, which carved L2
-  // from every other pass).  GCB_L2_PERSIST=<MB> overrides (0: no set-aside,
-  // the per-load range policy; "max": the device maximum).
+  // Persisting L2 set-aside for an access-policy window on the pull gather
+  // (gather.cu launch_block pins the head of the degree-ordered value slice):
+  // opt-in, GCB_L2_PERSIST=<MB> ("max": the device maximum).  At rmat:24 a
+  // 48 MB set-aside ran the step as fast as the default per-load range
+  // policy (7.186 vs 7.19 ms; 7.25 / 7.44 / 7.89 ms at 32 / 64 MB / maximum)
+  // but the pull launch then moved 1.75 GB of DRAM against 1.08 GB (ncu,
+  // profiles/r2_l2_window_attr.txt): the set-aside shrinks the L2 left for
+  // the slice's tail, the sums and the streams.  The kernel is request-bound,
+  // so the extra traffic costs no time today, but it is wasted bandwidth.
   if (ctx->persist_max > 0) {
     const char *env = getenv("GCB_L2_PERSIST");
-    const double mb = env && env[0] ? (strcmp(env, "max") == 0 ? -1.0 : atof(env)) : 48.0;
+    const double mb = env && env[0] ? (strcmp(env, "max") == 0 ? -1.0 : atof(env)) : 0.0;
     int64_t want = mb > 0 ? (int64_t)(mb * 1048576.0) : (mb < 0 ? ctx->persist_max : 0);
     if (want > ctx->persist_max) want = ctx->persist_max;
     if (want > 0) {

@@ -532,13 +532,14 @@ static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double 
   const double *hot_src = HOTBIT ? bg->hotval.p + b * bg->hot_k : vals + lo;
   // L2 residency of the cold gathers (north star (1)): on the degree-ordered
   // copy the block's value slice is sorted by out-degree, so its head holds
-  // the most-read cold values.  With the context's persisting set-aside (48 MB
-  // by default, ctx.cu) the launch carries an access-policy window over that
-  // head (below).  Without one, a range policy -- the per-instruction form of
-  // the window (createpolicy.range) -- marks the first kL2KeepMB of the slice
-  // evict_last and leaves the tail at normal priority; the two ran 7.186 vs
-  // 7.19 ms per step at rmat:24 (profiles/r2_l2_window_attr.txt).  For the
-  // range policy, marking the tail evict_first ran slower, as did a 16 MB head
+  // the most-read cold values.  By default a range policy -- the
+  // per-instruction form of an access-policy window (createpolicy.range) --
+  // marks the first kL2KeepMB of the slice evict_last and leaves the tail at
+  // normal priority.  With a persisting set-aside (GCB_L2_PERSIST=<MB>, ctx.cu)
+  // the launch carries a real access-policy window over that head instead
+  // (below): as fast at 48 MB (7.186 vs 7.19 ms per step at rmat:24) but 1.6x
+  // the DRAM traffic (profiles/r2_l2_window_attr.txt).  For the range policy,
+  // marking the tail evict_first ran slower, as did a 16 MB head
   // (profiles/r2_l2_window.txt).  GCB_L2_RANGE="<MB>:<mode>" overrides it (mode
   // 1: tail evict_first, 2: tail unchanged, 0: whole slice evict_last); the
   // hot-bit layout has no sorted slice and keeps evict_last.
@@ -555,10 +556,10 @@ static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double 
     if (mode && keep < total && total < (uint64_t(1) << 32))
       rp = RangePolicy{mode, (uint32_t)keep, (uint32_t)total};
   }
-  // North star (1): with a persisting set-aside in force (GCB_L2_PERSIST=<MB>)
-  // the head of a degree-ordered value slice -- its most-read cold values --
-  // is pinned by a launch access-policy window instead of the per-load range
-  // policy (measured against it in profiles/r2_l2_window_attr.txt).
+  // With a persisting set-aside in force (GCB_L2_PERSIST=<MB>) the head of a
+  // degree-ordered value slice -- its most-read cold values -- is pinned by a
+  // launch access-policy window instead of the per-load range policy
+  // (measured against it in profiles/r2_l2_window_attr.txt).
   const bool window = !HOTBIT && ctx->persist_set > 0 && ctx->window_max > 0;
   if (window) {
     uint64_t wbytes = (uint64_t)(hi - lo) * 8u;
@@ -577,7 +578,10 @@ static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double 
     attr[0].val.accessPolicyWindow.num_bytes = (size_t)wbytes;
     attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
     attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    // accesses past the window's hit fraction stay normal (streaming evicted
+    // the slice's tail early: ncu DRAM per launch 1.79 GB against 1.08 GB)
+    attr[0].val.accessPolicyWindow.missProp =
+        getenv("GCB_L2_WINDOW_STREAM") ? cudaAccessPropertyStreaming : cudaAccessPropertyNormal;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     GCB_CUDA(cudaLaunchKernelEx(&cfg, k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps, false>,
