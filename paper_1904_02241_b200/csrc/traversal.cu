@@ -36,7 +36,8 @@ __global__ void k_bfs_pull_block(int64_t Lb, const uint32_t *__restrict__ lro_b,
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Lb;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t v = id_map_b[i];
-    if (depth[v] != kInfDepth) continue;
+    // found in an earlier block of this level (blocks run in order), or visited
+    if (next[v] || depth[v] != kInfDepth) continue;
     const uint32_t e1 = lro_b[i + 1];
     for (uint32_t e = lro_b[i]; e < e1; ++e) {
       const uint32_t u = col_b[e];
