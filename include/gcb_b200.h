@@ -81,6 +81,9 @@ int gcb_ctx_sync(gcb_ctx *ctx);
 /* L2 facts the partitioner sizes blocks from (SURVEY 7 "hard parts") */
 int gcb_ctx_info(gcb_ctx *ctx, int64_t *num_sms, int64_t *l2_bytes,
                  int64_t *persist_max_bytes, int64_t *window_max_bytes);
+/* persisting-L2 set-aside this context made (GCB_L2_PERSIST; 0 = none, the
+ * pull gather then uses its per-load range policy instead of a window) */
+int gcb_ctx_l2_set_aside(gcb_ctx *ctx, int64_t *bytes);
 /* number of this library's kernel launches issued on ctx so far */
 int gcb_ctx_launch_count(gcb_ctx *ctx, int64_t *count);
 /* CUDA-event timing of kernel groups on the ctx stream (bench.py roofline):

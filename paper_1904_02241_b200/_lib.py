@@ -50,6 +50,7 @@ SIGNATURES = {
     "gcb_ctx_set_stream": ([c_vp, c_vp], c_int),
     "gcb_ctx_sync": ([c_vp], c_int),
     "gcb_ctx_info": ([c_vp, P_i64, P_i64, P_i64, P_i64], c_int),
+    "gcb_ctx_l2_set_aside": ([c_vp, P_i64], c_int),
     "gcb_ctx_launch_count": ([c_vp, P_i64], c_int),
     "gcb_ctx_set_profiling": ([c_vp, c_int], c_int),
     "gcb_ctx_read_profile": ([c_vp, P_dbl, P_i64], c_int),
@@ -216,8 +217,10 @@ class Context:
         vals = [c_i64() for _ in range(4)]
         check(self._lib.gcb_ctx_info(self.handle, *[ctypes.byref(v) for v in vals]))
         sms, l2, persist, window = (v.value for v in vals)
+        aside = c_i64()
+        check(self._lib.gcb_ctx_l2_set_aside(self.handle, ctypes.byref(aside)))
         return {"num_sms": sms, "l2_bytes": l2, "persist_max_bytes": persist,
-                "window_max_bytes": window}
+                "window_max_bytes": window, "persist_set_bytes": aside.value}
 
     def launches(self) -> int:
         v = c_i64()

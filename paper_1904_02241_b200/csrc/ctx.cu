@@ -177,6 +177,13 @@ int gcb_ctx_info(gcb_ctx *ctx, int64_t *num_sms, int64_t *l2_bytes, int64_t *per
   GCB_API_END
 }
 
+int gcb_ctx_l2_set_aside(gcb_ctx *ctx, int64_t *bytes) {
+  GCB_API_BEGIN
+  GCB_REQUIRE(ctx && bytes, "NULL argument");
+  *bytes = ctx->persist_set;
+  GCB_API_END
+}
+
 int gcb_ctx_launch_count(gcb_ctx *ctx, int64_t *count) {
   GCB_API_BEGIN
   GCB_REQUIRE(ctx && count, "NULL argument");
