@@ -1,0 +1,4 @@
+set -x
+O=gpurun_out/s4f
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "access_policy or sssp or SSSP" > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log; tail -3 $O/pytest.log
