@@ -49,6 +49,41 @@ __global__ void k_bfs_pull_block(int64_t Lb, const uint32_t *__restrict__ lro_b,
   }
 }
 
+// Every block's rows in one launch (the per-block launches of a pull level
+// were 8 small kernels with a gap each at rmat:24, W = 2^21).  Global row r
+// of block b reads lro[r + b] and the col arena from edge_starts[b]; rows
+// go in block order, so most rows of later blocks still see the next[] flags
+// their vertex got from an earlier block.
+constexpr int kMaxPullBlocks = 64;
+__global__ void k_bfs_pull_all(int64_t L, int B, const int64_t *__restrict__ row_starts,
+                               const int64_t *__restrict__ edge_starts,
+                               const uint32_t *__restrict__ lro, const uint32_t *__restrict__ id_map,
+                               const uint32_t *__restrict__ col, const uint32_t *__restrict__ front_bits,
+                               const int32_t *__restrict__ depth, uint8_t *__restrict__ next) {
+  __shared__ int64_t s_rs[kMaxPullBlocks + 1], s_es[kMaxPullBlocks + 1];
+  for (int i = threadIdx.x; i <= B; i += blockDim.x) {
+    s_rs[i] = row_starts[i];
+    s_es[i] = i < B ? edge_starts[i] : 0;
+  }
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < L;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int b = 0;
+    while (b + 1 < B && s_rs[b + 1] <= r) ++b;
+    const uint32_t v = id_map[r];
+    if (next[v] || depth[v] != kInfDepth) continue;
+    const uint32_t *col_b = col + s_es[b];
+    const uint32_t e1 = lro[r + b + 1];
+    for (uint32_t e = lro[r + b]; e < e1; ++e) {
+      const uint32_t u = col_b[e];
+      if (front_bits[u >> 5] >> (u & 31) & 1u) {
+        next[v] = 1;
+        break;
+      }
+    }
+  }
+}
+
 static gcb_blocked *default_pull_blocking(gcb_ctx *ctx, const gcb_csr *g,
                                           gcb_blocked **owned) {
   // traversal.py:186-187: partition_tocab(transpose(g), "pull", max(1, n // 8))
@@ -320,14 +355,23 @@ static void bfs_run(gcb_ctx *ctx, const gcb_csr *g, gcb_blocked *bg, int64_t sou
         after_launch(ctx, "k_bfs_push_eb");
       }
     } else {
-      for (int64_t b = 0; b < bg->B; ++b) {
-        const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
-        if (!Lb) continue;
-        const int64_t es = bg->h_edge_starts[b];
-        k_bfs_pull_block<<<grid_for(Lb, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-            Lb, bg->lro.p + rs + b, bg->id_map.p + rs, bg->col.p + es, F.bits.p, depth_dev,
-            F.next.p);
-        after_launch(ctx, "k_bfs_pull_block");
+      if (bg->B <= kMaxPullBlocks && !getenv("GCB_BFS_PULL_PER_BLOCK")) {
+        if (bg->L)
+          k_bfs_pull_all<<<grid_for(bg->L, 256, (int64_t)ctx->num_sms * 16), 256, 0,
+                           ctx->stream>>>(bg->L, (int)bg->B, bg->row_starts.p, bg->edge_starts.p,
+                                          bg->lro.p, bg->id_map.p, bg->col.p, F.bits.p, depth_dev,
+                                          F.next.p);
+        after_launch(ctx, "k_bfs_pull_all");
+      } else {
+        for (int64_t b = 0; b < bg->B; ++b) {
+          const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
+          if (!Lb) continue;
+          const int64_t es = bg->h_edge_starts[b];
+          k_bfs_pull_block<<<grid_for(Lb, 256, (int64_t)ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+              Lb, bg->lro.p + rs + b, bg->id_map.p + rs, bg->col.p + es, F.bits.p, depth_dev,
+              F.next.p);
+          after_launch(ctx, "k_bfs_pull_block");
+        }
       }
     }
     int64_t cnt = 0;

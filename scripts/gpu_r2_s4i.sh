@@ -1,0 +1,7 @@
+# BFS pull in one launch over all blocks: parity and spans A/B
+set -x
+O=gpurun_out/s4i
+mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "bfs or BFS or c6 or Traversal or bc or BC or rmat24_bfs" > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log; tail -2 $O/pytest.log
+timeout 600 python scripts/traversal_spans.py 7 > $O/one.txt 2>&1; tail -1 $O/one.txt
+GCB_BFS_PULL_PER_BLOCK=1 timeout 600 python scripts/traversal_spans.py 7 > $O/per.txt 2>&1; tail -1 $O/per.txt
