@@ -9,10 +9,10 @@ Every compute entry point runs on the B200 through libgcb_b200.so:
   storage-order adds, block-ordered merge, no FMA): results are bit-identical
   to the reference.  The default fast path reassociates the per-row sums and
   is NOT bitwise deterministic run to run: rows that span warp tiles and the
-  push / hybrid hub passes add with f64 atomics whose order varies, and the
-  hybrid pass's shared-memory hub table rounds every term to a multiple of
-  2^-62 (64-bit fixed point; PageRank values lie in [0, 1)).  Results stay
-  within 1e-12 relative of the reference (the bar is 1e-6).
+  plain push pass add with f64 atomics whose order varies.  The hybrid hub
+  pass rounds every term to a multiple of 2^-62 (64-bit fixed point; PageRank
+  values lie in [0, 1)) and sums in integers, so that part is order-free.
+  Results stay within 1e-12 relative of the reference (the bar is 1e-6).
 * the fine-grained operators (``process_block_pull``, ``process_block_push``,
   ``segment_row_sums``, ``accumulate_ranges``) default to ``exact=True`` --
   they are the reference's bit-pinned building blocks (test_kernels.py:196-206,
