@@ -661,8 +661,11 @@ __global__ void __launch_bounds__(256)
 // (ATOMS.CAST.SPIN) that serialises on the hottest hubs.  Sums stay below 1
 // (rank mass), so a CTA's slot cannot overflow; each term is rounded to
 // 2^-62 absolute, and integer adds make the slot order-independent.
-constexpr double kFixScale = 4611686018427387904.0;        // 2^62
-constexpr double kFixInv = 1.0 / 4611686018427387904.0;
+#ifndef GCB_FIX_BITS
+#define GCB_FIX_BITS 62  // experiment builds override (Makefile `variant`)
+#endif
+constexpr double kFixScale = (double)(1ull << GCB_FIX_BITS);  // 2^62
+constexpr double kFixInv = 1.0 / kFixScale;
 
 // 64-bit shared adds (f64 or u64) are CAS loops on sm_100 (ATOMS.CAST.SPIN);
 // 32-bit ATOMS.ADD is native.  A 64-bit fixed-point slot is therefore two
