@@ -64,10 +64,11 @@ __constant__ int c_abl;
 #define ABL(b) 0
 #endif
 
-template <bool HOTBIT, bool HINT = true>
+template <bool HOTBIT, bool HINT = true, bool LO0 = false>
 __device__ __forceinline__ double gather_one(const double *vals, uint32_t c, uint32_t lo,
                                              uint32_t hot, uint32_t s_hot, uint64_t pol) {
-  const uint32_t h = HOTBIT ? (c ^ kHotBit) : c - lo;
+  // LO0: the block's sources start at id 0 (block 0), so the slot is the id
+  const uint32_t h = HOTBIT ? (c ^ kHotBit) : (LO0 ? c : c - lo);
   double x;
   if (ABL(1) && h >= hot) return 0.0;
   if (HINT)
@@ -97,7 +98,7 @@ struct RangePolicy {
   uint32_t keep, total;
 };
 
-template <bool WGT, bool ASSIGN, bool HOTBIT, int NW, bool HINT = true>
+template <bool WGT, bool ASSIGN, bool HOTBIT, int NW, bool HINT = true, bool LO0 = false>
 __global__ void __launch_bounds__(NW * 32, 1)
     k_pull_hot(const uint32_t *__restrict__ col, const double *__restrict__ w,
                const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ id_map_b,
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     double v[V];
 #pragma unroll
     for (int k = 0; k < V; ++k)
-      v[k] = gather_one<HOTBIT, HINT>(vals, c[k], lo, (uint32_t)hot, s_hot_addr, pol_keep);
+      v[k] = gather_one<HOTBIT, HINT, LO0>(vals, c[k], lo, (uint32_t)hot, s_hot_addr, pol_keep);
     if (WGT) {
       double ww[V];
       ld_stream_f64x4(w + abase + lane * V, pol_stream, ww);
@@ -590,6 +591,14 @@ static void launch_block(gcb_ctx *ctx, gcb_blocked *bg, int64_t b, const double 
                                 (const uint32_t *)bg->rstart.p, (const uint32_t *)(bg->id_map.p + rs),
                                 (const uint32_t *)(bg->tile_row.p + tb), es, ee, bg->h_tile_t0[b], nt,
                                 (uint32_t)lo, hot, (uint32_t)Lb, hot_src, vals, out, rp));
+  } else if (!HOTBIT && lo == 0 && !getenv("GCB_NO_LO0")) {
+    ensure_smem_attrs(ctx, (const void *)k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps, true, true>,
+                      smem, pct > 100 ? 100 : pct);
+    k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps, true, true>
+        <<<(unsigned)(grid < 1 ? 1 : grid), kGWarps * 32, smem, ctx->stream>>>(
+            HOTBIT ? bg->xcol.p : bg->col.p, WGT ? bg->w.p : nullptr, bg->rstart.p,
+            bg->id_map.p + rs, bg->tile_row.p + tb, es, ee, bg->h_tile_t0[b], nt, (uint32_t)lo,
+            hot, (uint32_t)Lb, hot_src, vals, out, rp);
   } else {
     k_pull_hot<WGT, ASSIGN, HOTBIT, kGWarps>
         <<<(unsigned)(grid < 1 ? 1 : grid), kGWarps * 32, smem, ctx->stream>>>(
