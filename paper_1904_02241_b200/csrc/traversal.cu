@@ -668,35 +668,75 @@ __global__ void k_cc_flatten(int64_t n, uint32_t *parent) {
 
 // every edge (u, v), edge-balanced (a hub row no longer serialises on one
 // warp); after the sampling rounds most endpoints already point straight at
-// the giant root, so the common case is two reads and no atomics
-// src[e] = source row of edge e.  A warp takes 32 consecutive rows: one
-// coalesced load of their 33 offsets (the row-per-warp form waited out two
-// dependent offset loads per row: 1.0 ms at rmat:24), then the rows' runs are
-// written in turn, the lanes striding over each run.
-__global__ void k_cc_src(int64_t n, const int64_t *__restrict__ ro, uint32_t *__restrict__ src) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; u0 < n;
-       u0 += nw * 32) {
-    const int64_t my = u0 + lane <= n ? ro[u0 + lane] : 0;
-    const int64_t last = u0 + 32 <= n ? ro[u0 + 32] : ro[n];
-    const int rows = (int)(n - u0 < 32 ? n - u0 : 32);
-    for (int r = 0; r < rows; ++r) {
-      const int64_t s = __shfl_sync(0xffffffffu, my, r);
-      const int64_t e = r + 1 < 32 ? __shfl_sync(0xffffffffu, my, r + 1) : last;
-      for (int64_t k = s + lane; k < e; k += 32) src[k] = (uint32_t)(u0 + r);
-    }
+// the giant root, so the common case is two reads and no atomics.  A warp
+// takes a group of kCcGroup consecutive edges and walks them 32 at a time:
+// the lanes load the ends of the next 32 rows once, and each lane finds its
+// edge's row by a 5-step shuffle binary search over them.  No per-edge source
+// array: materialising src[] wrote and re-read 1.07 GB at rmat:24, and its
+// warp-per-32-rows writer (k_cc_src) took 0.82 ms behind the hub rows.
+constexpr int64_t kCcGroup = 1024;
+
+// grp_row[g] = the row holding edge g * kCcGroup (thread per row; the rows
+// of hub vertices cover several groups)
+__global__ void k_cc_group_rows(int64_t n, const int64_t *__restrict__ ro,
+                                uint32_t *__restrict__ grp_row) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = ro[u], e = ro[u + 1];
+    for (int64_t g = (s + kCcGroup - 1) / kCcGroup; g * kCcGroup < e; ++g) grp_row[g] = (uint32_t)u;
   }
 }
 
-__global__ void k_cc_edges(int64_t m, const uint32_t *__restrict__ src,
-                           const uint32_t *__restrict__ col, uint32_t *parent) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = src[e], v = col[e];
-    const uint32_t pu = __ldcg(parent + u), pv = __ldcg(parent + v);
-    if (pu == pv) continue;
-    uf_union(parent, pu, pv);
+__global__ void k_cc_edges(int64_t n, int64_t m, const int64_t *__restrict__ ro,
+                           const uint32_t *__restrict__ grp_row, const uint32_t *__restrict__ col,
+                           uint32_t *parent) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g * kCcGroup < m;
+       g += nw) {
+    int64_t base = g * kCcGroup;
+    const int64_t gend = base + kCcGroup < m ? base + kCcGroup : m;
+    // window: the ends of rows uw .. uw + 31 (one coalesced load), kept while
+    // it covers the edges; uw starts at the row holding edge `base`
+    uint32_t uw = grp_row[g];
+    auto ends = [&](uint32_t r0) {
+      return (int64_t)r0 + lane + 1 <= n ? __ldg(ro + r0 + lane + 1) : INT64_MAX;
+    };
+    int64_t rend = ends(uw), wend = __shfl_sync(FULL, rend, 31);
+    while (base < gend) {
+      // every window row ends at or before base (empty rows): the next 32
+      while (wend <= base) {
+        uw += 32;
+        rend = ends(uw);
+        wend = __shfl_sync(FULL, rend, 31);
+      }
+      // up to 64 edges per pass, two per lane, so two independent load
+      // chains are in flight
+      const int64_t lim = gend < wend ? gend : wend;
+      const int step = lim - base < 64 ? (int)(lim - base) : 64;
+      const int64_t p0 = base + lane, p1 = p0 + 32;
+      const bool ok0 = lane < step, ok1 = lane + 32 < step;
+      const uint32_t v0 = ok0 ? __ldcs(col + p0) : 0u, v1 = ok1 ? __ldcs(col + p1) : 0u;
+      // row of an edge: the first window row whose end exceeds it (per-lane
+      // shuffle binary search)
+      int lo0 = 0, hi0 = 31, lo1 = 0, hi1 = 31;
+#pragma unroll
+      for (int s = 0; s < 5; ++s) {
+        const int mid0 = (lo0 + hi0) >> 1, mid1 = (lo1 + hi1) >> 1;
+        const int64_t x0 = __shfl_sync(FULL, rend, mid0), x1 = __shfl_sync(FULL, rend, mid1);
+        if (x0 > p0) hi0 = mid0;
+        else lo0 = mid0 + 1;
+        if (x1 > p1) hi1 = mid1;
+        else lo1 = mid1 + 1;
+      }
+      const uint32_t u0 = uw + (uint32_t)lo0, u1 = uw + (uint32_t)lo1;
+      const uint32_t pu0 = ok0 ? __ldcg(parent + u0) : 0u, pv0 = ok0 ? __ldcg(parent + v0) : 0u;
+      const uint32_t pu1 = ok1 ? __ldcg(parent + u1) : 0u, pv1 = ok1 ? __ldcg(parent + v1) : 0u;
+      if (pu0 != pv0) uf_union(parent, pu0, pv0);
+      if (pu1 != pv1) uf_union(parent, pu1, pv1);
+      base += step;
+    }
   }
 }
 
@@ -886,11 +926,12 @@ int gcb_cc(gcb_ctx *ctx, const gcb_csr *g, uint32_t *labels_host, int64_t *num_c
       k_cc_flatten<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, parent.p);
       after_launch(ctx, "k_cc_flatten");
     }
-    DArray<uint32_t> src(g->m);
-    k_cc_src<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, g->ro.p, src.p);
-    after_launch(ctx, "k_cc_src");
-    k_cc_edges<<<grid_for(g->m, 256, (int64_t)ctx->num_sms * 32), 256, 0, ctx->stream>>>(
-        g->m, src.p, g->col.p, parent.p);
+    const int64_t groups = (g->m + kCcGroup - 1) / kCcGroup;
+    DArray<uint32_t> grp_row(groups);
+    k_cc_group_rows<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, g->ro.p, grp_row.p);
+    after_launch(ctx, "k_cc_group_rows");
+    k_cc_edges<<<grid_for(groups * 32, 256, (int64_t)ctx->num_sms * 64), 256, 0, ctx->stream>>>(
+        n, g->m, g->ro.p, grp_row.p, g->col.p, parent.p);
     after_launch(ctx, "k_cc_edges");
   }
   k_cc_compress<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, parent.p, cnt.p);
