@@ -15,6 +15,8 @@
 // (k_permute_in / k_permute_out).  Sums differ from the reference's only by
 // reassociation (the fast-mode contract, <= 1e-6 relative); the exact mode
 // never uses this layout.
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -123,11 +125,11 @@ __global__ void k_order_keys(int64_t n, const uint32_t *__restrict__ deg,
   }
 }
 
-// Tiering: the copy costs a few passes over the edges (tens of ms at
-// rmat:24) and saves ~0.07 ms per iteration there, so it pays only on a graph
-// that stays resident.  A graph is promoted once it has run
-// GCB_RELABEL_AFTER fast-mode iterations (default 20; 0 = immediately); a
-// graph uploaded for one short call never is.
+// Tiering: the copy costs a few passes over the edges (~55 ms at rmat:24)
+// and saves ~0.2 ms per iteration there, so it pays only on a graph that
+// stays resident.  A graph is promoted once it has run GCB_RELABEL_AFTER
+// fast-mode iterations (default 256; 0 = immediately); a graph uploaded for
+// one short call never is.
 // ---------------------------------------------------------------------------
 // Hybrid split of the degree-ordered copy.  Every cold gather of the pull
 // kernel costs one L1->XBAR request (gather.cu), but an edge from a cold
@@ -271,13 +273,15 @@ bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters) {
   const char *env = getenv("GCB_NO_RELABEL");
   if (env && env[0] && env[0] != '0') return false;
   if (bg->rl) return true;
-  // Ski rental: building the copy costs ~350 ms at rmat:24 (up to 1.4 s
-  // while the memory pool first grows) and saves ~0.057 ms per iteration, so
-  // it pays only after ~6000 iterations; promoting after 4096 keeps any
-  // workload within ~2.5x of the better choice.  Long-running jobs (and
-  // bench.py, which builds it in its untimed setup) get the steady state.
+  // Ski rental: building the copy (permutation, renumbered edges, hybrid
+  // split, pull CSR, both partitions) costs 53-62 ms at rmat:24 and saves
+  // ~0.20 ms per iteration (hot-bit 11.6 vs promoted 9.6 ms per 10-iteration
+  // call; profiles/r2_promotion_trace.txt, GCB_TRACE_PROMO=1), so it pays after
+  // ~270-310 iterations.  Promoting once 256 fast iterations have been asked
+  // for keeps any workload within ~2x of the better choice; long-running jobs
+  // (and bench.py, which builds it in its untimed setup) get the steady state.
   const char *after = getenv("GCB_RELABEL_AFTER");
-  const int64_t threshold = after ? atoll(after) : 4096;
+  const int64_t threshold = after ? atoll(after) : 256;
   if (bg->fast_iters >= threshold) return true;
   bg->fast_iters += upcoming_iters;
   return false;
@@ -319,9 +323,32 @@ gcb_blocked *ensure_exact_pull(gcb_ctx *ctx, gcb_blocked *bg) {
   return bg->exact_pull;
 }
 
+// GCB_TRACE_PROMO=1: synchronise after each stage of the promotion build and
+// print its wall time to stderr (the stage costs behind the ski-rental threshold)
+struct PromoTrace {
+  gcb_ctx *ctx;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PromoTrace(gcb_ctx *c) : ctx(c) {
+    const char *e = getenv("GCB_TRACE_PROMO");
+    on = e && e[0] && e[0] != '0';
+    if (on) { sync(ctx); t = std::chrono::steady_clock::now(); }
+  }
+  void mark(const char *stage) {
+    if (!on) return;
+    sync(ctx);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[promo] %-28s %8.2f ms\n", stage,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
   if (bg->rl) return bg->rl;
+  PromoTrace tr(ctx);
   ensure_derived(ctx, bg);
+  tr.mark("derived tables");
   const int64_t n = bg->n, m = bg->m;
   // 1. permutation: stable sort of (deg desc, id asc)
   bg->rl_perm.alloc(n);
@@ -357,6 +384,7 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
     n_live = (int64_t)hc[0];
     n_conn = (int64_t)hc[1];
   }
+  tr.mark("permutation");
   // 2. renumbered edge list (destination, source) from the arenas
   gcb_csr *csr = nullptr;
   {
@@ -373,6 +401,7 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
     // a push blocking's rows are sources: the copy is always the pull
     // (destination-row) form, so push PageRank runs the same pipeline
     if (bg->direction == 1) std::swap(rows, cols);
+    tr.mark("renumbered edges");
     // 3. split off the edges whose source misses its block's hot prefix but
     //    whose destination is a hub (hybrid_split), then the canonical CSR of
     //    the rest of the renumbered transpose and the same TOCAB cut
@@ -383,6 +412,7 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
     if (hybrid_enabled()) {
       m_pull = hybrid_split(ctx, n, m, bg->width, rows, cols, w, wpull, &push_csr);
       if (push_csr && bg->weighted) w = wpull.p;  // split: the pull edges' own weights
+      tr.mark("hybrid split (+ push csr)");
     }
     try {
       csr = csr_from_device_edges(ctx, n, m_pull, rows.p, cols.p, w);
@@ -390,6 +420,7 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
       if (push_csr) gcb_csr_destroy(push_csr);
       throw;
     }
+    tr.mark("pull csr");
     if (push_csr) {
       try {
         bg->pending_hybrid = partition_device(ctx, push_csr, 1, n);  // one block: every hub slot
@@ -399,10 +430,12 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
         throw;
       }
       gcb_csr_destroy(push_csr);
+      tr.mark("push partition");
     }
   }
   try {
     gcb_blocked *rl = partition_device(ctx, csr, 0, bg->width);
+    tr.mark("pull partition");
     rl->is_relabeled = true;
     rl->n_live = n_live;
     rl->n_conn = n_conn;
@@ -425,6 +458,7 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
   }
   gcb_csr_destroy(csr);
   sync(ctx);
+  tr.mark("push exec table, degrees");
   return bg->rl;
 }
 
