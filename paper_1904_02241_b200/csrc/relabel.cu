@@ -38,20 +38,40 @@ __global__ void k_invert(int64_t n, const uint32_t *__restrict__ inv, uint32_t *
 }
 
 // Edges of one block, renumbered: rows (destinations) and cols (sources).
-// One warp per local row.
-__global__ void k_relabel_block(int64_t Lb, const uint32_t *__restrict__ lro_b,
-                                const uint32_t *__restrict__ id_map_b,
-                                const uint32_t *__restrict__ col_b, const uint32_t *__restrict__ perm,
-                                uint32_t *__restrict__ rows_out, uint32_t *__restrict__ cols_out) {
+// The source ids are renumbered edge-parallel (k_relabel_cols: four
+// independent perm lookups per thread in flight); the row ids are written by
+// one warp per local row (k_relabel_rows: stores only), which also adds the
+// row's length to the destination's in-degree (one atomic per local row
+// instead of one per edge) when the hybrid split needs it.  One warp per row
+// doing both took 8 ms at rmat:24 (profiles/r2_promotion_trace.txt): its
+// per-edge perm gathers sat behind the row's dependent lro -> id_map -> perm
+// chain.
+__global__ void k_relabel_cols(int64_t cnt, const uint32_t *__restrict__ col_b,
+                               const uint32_t *__restrict__ perm, uint32_t *__restrict__ cols_out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += 4 * stride) {
+    uint32_t c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = i + k * stride < cnt ? col_b[i + k * stride] : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = i + k * stride < cnt ? __ldg(perm + c[k]) : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k * stride < cnt) cols_out[i + k * stride] = c[k];
+  }
+}
+
+__global__ void k_relabel_rows(int64_t Lb, const uint32_t *__restrict__ lro_b,
+                               const uint32_t *__restrict__ id_map_b,
+                               const uint32_t *__restrict__ perm, uint32_t *__restrict__ rows_out,
+                               uint32_t *__restrict__ indeg) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Lb; r += nw) {
     const uint32_t s = lro_b[r], e = lro_b[r + 1];
     const uint32_t d = perm[id_map_b[r]];
-    for (uint32_t i = s + lane; i < e; i += 32) {
-      rows_out[i] = d;
-      cols_out[i] = perm[col_b[i]];
-    }
+    if (indeg && lane == 0) atomicAdd(indeg + d, e - s);
+    for (uint32_t i = s + lane; i < e; i += 32) rows_out[i] = d;
   }
 }
 
@@ -125,7 +145,7 @@ __global__ void k_order_keys(int64_t n, const uint32_t *__restrict__ deg,
   }
 }
 
-// Tiering: the copy costs a few passes over the edges (~55 ms at rmat:24)
+// Tiering: the copy costs a few passes over the edges (~42 ms at rmat:24)
 // and saves ~0.2 ms per iteration there, so it pays only on a graph that
 // stays resident.  A graph is promoted once it has run GCB_RELABEL_AFTER
 // fast-mode iterations (default 256; 0 = immediately); a graph uploaded for
@@ -216,19 +236,27 @@ __global__ void k_split_edges(int64_t m, const uint32_t *__restrict__ flag, cons
 
 // rows/cols (renumbered transpose edges, in place) keep the pull edges;
 // returns their count and the push CSR of the split-off edges
+// indeg (optional): in-degrees of the row ids, already counted by the caller
+// (consumed: the sort below reuses its storage)
 static int64_t hybrid_split(gcb_ctx *ctx, int64_t n, int64_t m, int64_t width,
                             DArray<uint32_t> &rows, DArray<uint32_t> &cols, const double *w,
-                            DArray<double> &w_pull, gcb_csr **push_csr) {
+                            DArray<double> &w_pull, gcb_csr **push_csr,
+                            DArray<uint32_t> *indeg = nullptr) {
   *push_csr = nullptr;
   const int64_t hs = hot_capacity(ctx);
   const int64_t hd = hybrid_hub_slots(ctx);
   if (m == 0 || hs <= 0 || hd <= 0 || width <= hs) return m;  // whole slices are hot already
   DArray<uint8_t> hot_dst(n);
   {
-    DArray<uint32_t> k1(n), k2(n), v1(n), v2(n);
-    GCB_CUDA(cudaMemsetAsync(k1.p, 0, n * sizeof(uint32_t), ctx->stream));
-    k_count_u32<<<grid_for(m, 256, 65536), 256, 0, ctx->stream>>>(m, rows.p, k1.p);
-    after_launch(ctx, "k_count_u32");
+    DArray<uint32_t> k1, k2(n), v1(n), v2(n);
+    if (indeg && indeg->p && indeg->n >= (size_t)n) {
+      k1 = std::move(*indeg);
+    } else {
+      k1.alloc(n);
+      GCB_CUDA(cudaMemsetAsync(k1.p, 0, n * sizeof(uint32_t), ctx->stream));
+      k_count_u32<<<grid_for(m, 256, 65536), 256, 0, ctx->stream>>>(m, rows.p, k1.p);
+      after_launch(ctx, "k_count_u32");
+    }
     k_iota_u32<<<grid_for(n, 256, 65536), 256, 0, ctx->stream>>>(n, v1.p);
     after_launch(ctx, "k_iota_u32");
     uint32_t *rk = nullptr, *rv = nullptr;
@@ -274,10 +302,11 @@ bool relabel_enabled(gcb_blocked *bg, uint32_t flags, int64_t upcoming_iters) {
   if (env && env[0] && env[0] != '0') return false;
   if (bg->rl) return true;
   // Ski rental: building the copy (permutation, renumbered edges, hybrid
-  // split, pull CSR, both partitions) costs 53-62 ms at rmat:24 and saves
+  // split, pull CSR, both partitions) costs 41-43 ms at rmat:24 once the
+  // memory pool has grown (53-62 ms before the edge-parallel relabel) and saves
   // ~0.20 ms per iteration (hot-bit 11.6 vs promoted 9.6 ms per 10-iteration
   // call; profiles/r2_promotion_trace.txt, GCB_TRACE_PROMO=1), so it pays after
-  // ~270-310 iterations.  Promoting once 256 fast iterations have been asked
+  // ~200-215 iterations.  Promoting once 256 fast iterations have been asked
   // for keeps any workload within ~2x of the better choice; long-running jobs
   // (and bench.py, which builds it in its untimed setup) get the steady state.
   const char *after = getenv("GCB_RELABEL_AFTER");
@@ -389,14 +418,23 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
   gcb_csr *csr = nullptr;
   {
     DArray<uint32_t> rows(m), cols(m);
+    // in-degrees of the renumbered destinations for the hybrid split (a pull
+    // blocking's rows are its destinations)
+    DArray<uint32_t> indeg;
+    if (hybrid_enabled() && bg->direction == 0) {
+      indeg.alloc(n);
+      GCB_CUDA(cudaMemsetAsync(indeg.p, 0, n * sizeof(uint32_t), ctx->stream));
+    }
     for (int64_t b = 0; b < bg->B; ++b) {
       const int64_t rs = bg->h_row_starts[b], Lb = bg->h_row_starts[b + 1] - rs;
-      const int64_t es = bg->h_edge_starts[b];
+      const int64_t es = bg->h_edge_starts[b], eb = bg->h_edge_starts[b + 1] - es;
       if (Lb == 0) continue;
-      k_relabel_block<<<grid_for(Lb * 32, 256, 65536), 256, 0, ctx->stream>>>(
-          Lb, bg->lro.p + rs + b, bg->id_map.p + rs, bg->col.p + es, bg->rl_perm.p, rows.p + es,
-          cols.p + es);
-      after_launch(ctx, "k_relabel_block");
+      k_relabel_cols<<<grid_for((eb + 3) / 4, 256, (int64_t)64 * ctx->num_sms), 256, 0,
+                       ctx->stream>>>(eb, bg->col.p + es, bg->rl_perm.p, cols.p + es);
+      after_launch(ctx, "k_relabel_cols");
+      k_relabel_rows<<<grid_for(Lb * 32, 256, 65536), 256, 0, ctx->stream>>>(
+          Lb, bg->lro.p + rs + b, bg->id_map.p + rs, bg->rl_perm.p, rows.p + es, indeg.p);
+      after_launch(ctx, "k_relabel_rows");
     }
     // a push blocking's rows are sources: the copy is always the pull
     // (destination-row) form, so push PageRank runs the same pipeline
@@ -410,7 +448,7 @@ gcb_blocked *ensure_relabeled(gcb_ctx *ctx, gcb_blocked *bg) {
     const double *w = bg->weighted ? bg->w.p : nullptr;
     DArray<double> wpull;
     if (hybrid_enabled()) {
-      m_pull = hybrid_split(ctx, n, m, bg->width, rows, cols, w, wpull, &push_csr);
+      m_pull = hybrid_split(ctx, n, m, bg->width, rows, cols, w, wpull, &push_csr, &indeg);
       if (push_csr && bg->weighted) w = wpull.p;  // split: the pull edges' own weights
       tr.mark("hybrid split (+ push csr)");
     }
