@@ -542,7 +542,12 @@ __global__ void __launch_bounds__(256, 4)
     }
     long long du[V];
 #pragma unroll
-    for (int k = 0; k < V; ++k) du[k] = ((fm >> k) & 1u) ? __ldcg(dist + c[k]) : LLONG_MAX;
+    // through L1 (block 0's hub sources are read by many tiles of a CTA: 6.0 ->
+    // 5.8 ms at rmat:24, profiles/r2_sssp_dist_l1_ab.txt).  A line cached before
+    // another CTA lowered dist[u] in this launch gives an older, larger distance:
+    // still a path length, and the improved u is in the next frontier anyway,
+    // so the fixed point (unique shortest distances) is unchanged.
+    for (int k = 0; k < V; ++k) du[k] = ((fm >> k) & 1u) ? __ldg(dist + c[k]) : LLONG_MAX;
     long long cand[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) {
