@@ -506,7 +506,9 @@ def run_ours(args):
                 "saving_ms_per_iteration": round(saving, 4),
                 "break_even_iterations": round(build / saving) if saving > 0 else None,
                 "note": "wall time of the first warm-up call over the later ones: derived "
-                        "tables of the uploaded graph + the degree-ordered build"}
+                        "tables of the uploaded graph + the degree-ordered build, including "
+                        "the memory pool's first growth in a fresh process (the build alone: "
+                        "41-43 ms at rmat:24, profiles/r2_promotion_trace.txt)"}
 
     # ---- e2e: public host-buffer API, arenas from pinned memory each step ----
     e2e = None
